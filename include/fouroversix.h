@@ -1,0 +1,159 @@
+/*
+ * fouroversix.h -- C ABI of the B200-native Four Over Six (4/6) NVFP4 path.
+ *
+ * Library: paper_2512_02010_b200/libfouroversix.so (sm_100a).  Plain pointers
+ * and sizes only; every pointer named d_* or documented "device" is CUDA
+ * device memory owned by the caller.  The library never allocates or frees
+ * caller memory; all work is enqueued on `stream` and is asynchronous.
+ * Functions return F46_OK (0) or a negative F46_ERR_* code.
+ *
+ * Reference interface each entry point replaces (paths under
+ * /root/reference/pkg/src/fp4emu/):
+ *   f46_amax            blockquant.py:218-219  (max|X| inside compute_tensor_scale;
+ *                                               non-finite check of _validated :197-198)
+ *   f46_quantize        blockquant.py:334-360  quantize_tensor (fixed6 / fixed4)
+ *                       adaptive.py:83-101     quantize_tensor_adaptive (4/6, MSE rule)
+ *                       blockquant.py:215-222  compute_tensor_scale (alpha, in the prologue)
+ *   f46_quantize_2d     transforms.py:134-179  quantize_weights_2d (16x16 tiles)
+ *   f46_dequantize      blockquant.py:363-376  dequantize_tensor
+ *   f46_gemm_nvfp4      qlinear.py:74-93       emulated_fp4_matmul(aq, bq, transpose_b=True)
+ *
+ * Data layout written by f46_quantize for a tensor viewed as [rows, cols]
+ * (cols = last dimension, 16-element blocks along it, nb = ceil(cols/16)):
+ *   codes      uint8 [rows][nb*8]: two E2M1 codes per byte, the even element
+ *              in the low nibble (tensor_io.py:118-123); tail pads are 0.
+ *   scales_tc  E4M3 block scales in the tcgen05 block-scaled-MMA layout:
+ *              128-row x 4-block tiles of 512 bytes,
+ *              offset(r, kb) = ((r/128)*ceil(nb/4) + kb/4)*512
+ *                              + (r%32)*16 + ((r%128)/32)*4 + kb%4;
+ *              size f46_scales_tc_bytes(rows, cols).
+ *   scales_rm  optional uint8 [rows][nb] (the reference's scale_codes layout).
+ *   pick4      optional uint8 [rows][nb]: 1 where the M=4 candidate was kept
+ *              (adaptive.py:77-80; parity/diagnostics only).
+ */
+#ifndef FOUROVERSIX_H_
+#define FOUROVERSIX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* f46_stream_t; /* a cudaStream_t */
+
+/* return codes */
+#define F46_OK 0
+#define F46_ERR_INVALID_ARG (-1) /* -> InvalidInputError in the Python mirror */
+#define F46_ERR_CONFIG (-2)      /* -> ConfigError */
+#define F46_ERR_UNSUPPORTED (-3) /* shape/alignment the kernel does not take */
+#define F46_ERR_CUDA (-4)        /* launch failure -> RuntimeError */
+
+/* element types */
+#define F46_DT_F32 0
+#define F46_DT_BF16 1
+#define F46_DT_F64 2
+
+/* scale modes (QuantConfig.scale_mode, blockquant.py:59) */
+#define F46_FIXED6 0
+#define F46_FIXED4 1
+#define F46_ADAPTIVE 2
+
+/* adaptive selection rules (QuantConfig.rule, adaptive.py:46) */
+#define F46_RULE_MSE 0
+#define F46_RULE_L1 1
+#define F46_RULE_ABSMAX 2
+
+/* scale layouts for f46_dequantize */
+#define F46_SCALES_TC 0
+#define F46_SCALES_RM 1
+
+/* bits of the device flags word */
+#define F46_FLAG_NONFINITE 1u   /* a non-finite input element was seen */
+#define F46_FLAG_NAN_SCALE 2u   /* dequantize saw an E4M3 NaN scale code */
+
+/* Bytes of the scales_tc buffer for a [rows, cols] tensor. */
+size_t f46_scales_tc_bytes(int64_t rows, int64_t cols);
+
+/* Bytes of the packed code buffer: rows * ceil(cols/16) * 8. */
+size_t f46_codes_bytes(int64_t rows, int64_t cols);
+
+/*
+ * Tensor-wide max|x| (blockquant.py:218-219).  Folds into *d_amax with an
+ * order-independent atomic max on the float64 bit pattern, so the caller
+ * zeroes d_amax once and may call this for several shards; a non-finite
+ * element leaves d_amax >= +inf (checked by the caller / quantize prologue).
+ *   x       device, n elements of `dtype`
+ *   d_amax  device double[1]
+ */
+int f46_amax(const void* x, int dtype, int64_t n, double* d_amax, f46_stream_t stream);
+
+/*
+ * 1-D NVFP4 quantization, 16-element blocks along the last dimension.
+ *   mode/rule      F46_FIXED6 | F46_FIXED4 | F46_ADAPTIVE, F46_RULE_*
+ *   mcap           M_fp4 * fp8_cap of QuantConfig (2688, 1792, 1536, 1024)
+ *   d_amax         device double[1] from f46_amax (+ allreduce MAX when
+ *                  sharded); ignored when alpha_override > 0
+ *   alpha_override > 0: use this tensor scale (blockquant.py:323-326)
+ *   d_alpha_out    device double[1]: the resolved alpha (nullable)
+ *   d_flags        device uint32[1]: F46_FLAG_* are OR-ed in (nullable)
+ * Outputs as described in the header comment; scales_rm / pick4 nullable.
+ */
+int f46_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int mode, int rule,
+                 double mcap, const double* d_amax, double alpha_override, uint8_t* codes,
+                 uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, double* d_alpha_out,
+                 uint32_t* d_flags, f46_stream_t stream);
+
+/*
+ * 2-D 16x16-tile quantization of a [R, C] weight (transforms.py:134-179):
+ * one E4M3 scale per tile (written to every row of the tile in both scale
+ * layouts), FP4 codes in the same packed layout.  W and W^T quantized this
+ * way are transposes of each other.
+ */
+int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, int rule,
+                    double mcap, const double* d_amax, double alpha_override, uint8_t* codes,
+                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, double* d_alpha_out,
+                    uint32_t* d_flags, f46_stream_t stream);
+
+/*
+ * Dequantize (blockquant.py:363-376): out = decode_fp4(code) * alpha * decode(scale).
+ *   scales       scales_tc (scale_layout = F46_SCALES_TC) or scales_rm (F46_SCALES_RM)
+ *   d_alpha      device double[1]
+ *   out          device [rows][cols] of out_dtype (F46_DT_F32: the exact value
+ *                rounded once to float32; F46_DT_BF16: rounded once to bf16;
+ *                F46_DT_F64: the exact value)
+ * A NaN scale code sets F46_FLAG_NAN_SCALE in d_flags.
+ */
+int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout,
+                   const double* d_alpha, int64_t rows, int64_t cols, void* out, int out_dtype,
+                   uint32_t* d_flags, f46_stream_t stream);
+
+/*
+ * Block-scaled NVFP4 GEMM on tcgen05 (kind::mxf4nvf4, E4M3 scales, 16-blocks):
+ *   C[M,N] = alpha_a * alpha_b * sum_k A[m,k] * B[n,k]
+ * A and B are both K-major f46_quantize outputs ("TN": qlinear.py:74-93 with
+ * transpose_b=True).  K must be a multiple of 64 (pad with zero blocks);
+ * M, N arbitrary.  C is row-major [M][ldc] of c_dtype (F46_DT_F32 or F46_DT_BF16).
+ */
+int f46_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_scales_tc, const double* d_alpha_a,
+                   const uint8_t* b_codes, const uint8_t* b_scales_tc, const double* d_alpha_b,
+                   int64_t M, int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                   f46_stream_t stream);
+
+/* Grouped (MoE-style) variant: `groups` independent GEMMs of one shape whose
+ * operands are packed back to back (stride = one operand's buffer size). */
+int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
+                           const double* d_alpha_a, const uint8_t* b_codes,
+                           const uint8_t* b_scales_tc, const double* d_alpha_b, int64_t M,
+                           int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                           f46_stream_t stream);
+
+/* Human-readable build info ("sm_100a ..."). */
+const char* f46_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FOUROVERSIX_H_ */

@@ -1,0 +1,172 @@
+"""GPU parity of the 4/6 quantize / dequantize path against the oracle.
+
+Every comparison is bit-exact: FP4 codes (packed), E4M3 scales, the per-block
+4-vs-6 choice and alpha; dequantized float64 values are exact and float32
+values are the exact value rounded once (np.float32 of the reference).
+Calls go through the package API -> C ABI (libfouroversix.so).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2512_02010_b200 as f46
+from oracle import oracle as O
+from tests.golden_util import opt, quant_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES = quant_cases()
+
+
+def to_torch(x: np.ndarray) -> torch.Tensor:
+    if x.dtype == np.uint16:
+        return torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run(x_t, mode, rule="mse", alpha=None, fp8_cap=None):
+    kw = dict(want_rowmajor=True, want_pick4=True)
+    if mode == "adaptive":
+        return f46.quantize_tensor_adaptive(x_t, f46.QuantConfig(scale_mode="adaptive", rule=rule),
+                                            alpha=alpha, **kw)
+    cfg = f46.QuantConfig(scale_mode=mode, **({} if fp8_cap is None else {"fp8_cap": fp8_cap}))
+    return f46.quantize_tensor(x_t, cfg, alpha=alpha, **kw)
+
+
+def assert_same(q, ref, rows):
+    assert q.alpha == ref["alpha"]
+    assert np.array_equal(q.scales_rm.cpu().numpy(), ref["scales"].reshape(rows, -1))
+    got = q.packed_codes.cpu().numpy()
+    bad = np.argwhere(got != ref["codes"])
+    assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[:4].tolist()}"
+    assert np.array_equal(q.pick4.cpu().numpy(), ref["pick4"].reshape(rows, -1))
+
+
+@pytest.mark.parametrize("name,rec", CASES, ids=[c[0] for c in CASES])
+def test_golden_fixture(name, rec):
+    x = rec["x"]
+    cols = x.shape[-1]
+    rows = x.size // cols
+    q = run(to_torch(x), str(rec["mode"]), str(rec["rule"]), opt(rec["alpha_override"]),
+            opt(rec["fp8_cap"]))
+    assert q.shape == tuple(x.shape)
+    assert_same(q, rec, rows)
+    # tcgen05-layout scales agree with the row-major view
+    assert np.array_equal(f46.blockquant.tc_to_rowmajor(q.scales_tc, rows, q.nblocks_per_row).cpu().numpy(),
+                          rec["scales"].reshape(rows, -1))
+    if "deq" in rec:
+        d64 = f46.dequantize_tensor(q, torch.float64).cpu().numpy().reshape(-1)
+        assert np.array_equal(d64, rec["deq"])
+        d32 = f46.dequantize_tensor(q, torch.float32).cpu().numpy().reshape(-1)
+        assert np.array_equal(d32, rec["deq"].astype(np.float32))
+
+
+def bf16_randn(shape, seed, std=1.0):
+    g = torch.Generator().manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * std).to(torch.bfloat16)
+
+
+def bits(x: torch.Tensor) -> np.ndarray:
+    return x.view(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6", "fixed4"])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_c1_4096sq_bf16_bit_exact(mode, seed):
+    """Config 1: 4096x4096 Gaussian BF16 (seed 2 has amax 5.75 -> alpha inexact)."""
+    x = bf16_randn((4096, 4096), seed)
+    q = run(x.cuda(), mode)
+    ref = O.quantize(bits(x), mode)
+    assert_same(q, ref, 4096)
+
+
+@pytest.mark.parametrize("shape", [(4096, 14336), (14336, 4096)])
+def test_c2_llama_weight_shapes(shape):
+    """Config 2: Llama-3-8B linear weights, N(0, 0.02^2) BF16."""
+    x = bf16_randn(shape, 7, std=0.02)
+    q = run(x.cuda(), "adaptive")
+    ref = O.quantize(bits(x), "adaptive")
+    assert_same(q, ref, shape[0])
+
+
+def test_fp32_input_bit_exact():
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(1024, 1536, generator=g) * 3
+    q = run(x.cuda(), "adaptive")
+    ref = O.quantize(x.numpy(), "adaptive")
+    assert_same(q, ref, 1024)
+
+
+@pytest.mark.parametrize("shape", [(5,), (3, 7), (2, 3, 40), (17, 33), (300, 80), (129, 4160)])
+def test_ragged_shapes(shape):
+    x = bf16_randn(shape, 3)
+    q = run(x.cuda(), "adaptive")
+    x2 = bits(x).reshape(-1, shape[-1])
+    ref = O.quantize(x2, "adaptive")
+    assert_same(q, ref, x2.shape[0])
+
+
+def test_nonfinite_rejected():
+    x = torch.randn(64, 64).to(torch.bfloat16)
+    x[3, 5] = float("inf")
+    with pytest.raises(f46.InvalidInputError):
+        run(x.cuda(), "adaptive")
+    x[3, 5] = float("nan")
+    with pytest.raises(f46.InvalidInputError):
+        run(x.cuda(), "adaptive", alpha=1.0)
+
+
+def test_idempotent_requantization():
+    # test_blockquant.py:182-189, on the GPU
+    x = (bf16_randn((256, 512), 13) * 2.5).float()
+    q1 = f46.quantize_tensor(x.cuda(), f46.QuantConfig())
+    q2 = f46.quantize_tensor(f46.dequantize_tensor(q1, torch.float64), f46.QuantConfig())
+    assert q1 == q2
+
+
+def test_alpha_override_validation():
+    x = torch.ones(1, 16).cuda()
+    with pytest.raises(f46.InvalidInputError):
+        f46.quantize_tensor(x, f46.QuantConfig(), alpha=-1.0)
+    with pytest.raises(f46.InvalidInputError):
+        f46.quantize_tensor(x, f46.QuantConfig(), alpha=float("inf"))
+
+
+def f64_to_bf16_bits(f: np.ndarray) -> np.ndarray:
+    """Round float64 to bf16 once (RNE): round-to-odd to float32, then RNE."""
+    f = np.asarray(f, np.float64)
+    rn = f.astype(np.float32)
+    away = np.abs(rn.astype(np.float64)) > np.abs(f)
+    rz = np.where(away, np.nextafter(rn, np.float32(0)), rn)
+    b = rz.view(np.uint32).copy()
+    b |= (rz.astype(np.float64) != f).astype(np.uint32)
+    return ((b.astype(np.uint64) + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def test_dequant_bf16_is_single_rounding():
+    x = bf16_randn((512, 1024), 21)
+    q = run(x.cuda(), "adaptive")
+    d64 = f46.dequantize_tensor(q, torch.float64).cpu().numpy()
+    d16 = f46.dequantize_tensor(q, torch.bfloat16).cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(d16, f64_to_bf16_bits(d64))
+
+
+def test_nan_scale_rejected_on_dequant():
+    q = f46.QuantizedTensor(shape=(16,), fmt="nvfp4", alpha=1.0,
+                            scale_codes=np.array([[0x7F]], dtype=np.uint8),
+                            codes=np.zeros(16, dtype=np.uint8))
+    with pytest.raises(f46.InvalidInputError):
+        f46.dequantize_tensor(q)
+
+
+def test_reference_style_float64_inputs():
+    # the reference's own tests feed float64 Gaussians; the exact path takes them
+    rng = np.random.Generator(np.random.Philox(3))
+    X = rng.standard_normal((8, 48))
+    q = f46.quantize_tensor(X, f46.QuantConfig())
+    ref = O.quantize(X, "fixed6")
+    assert q.alpha == ref["alpha"]
+    assert np.array_equal(q.packed_codes.cpu().numpy(), ref["codes"])
+    D = f46.dequantize_tensor(q, torch.float64).cpu().numpy()
+    assert np.array_equal(D, O.dequantize(ref["codes"], ref["scales"], ref["alpha"], 8, 48))
