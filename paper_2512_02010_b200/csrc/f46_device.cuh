@@ -282,6 +282,11 @@ struct TensorConsts {
   int force_exact;                   // alpha outside the fast path's range
 };
 
+// Relative half-width of the brackets.  Every f32 quantity below carries at
+// most ~2^-21.7 relative error (one approximate reciprocal, <= 1 ulp, plus
+// three RN roundings), so x*r_lo < x/(alpha*m) < x*r_hi strictly.
+#define F46_BRACKET 0x1p-17f
+
 __device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, int dtype) {
   TensorConsts t;
   t.alpha_d = alpha_d;
@@ -291,22 +296,29 @@ __device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, in
                   rule != RULE_MSE || dtype == DT_F64;
   const float r6 = (float)(1.0 / (alpha_d * 6.0));
   const float r4 = (float)(1.0 / (alpha_d * 4.0));
-  t.r6_lo = r6 * (1.0f - 0x1p-18f);
-  t.r6_hi = r6 * (1.0f + 0x1p-18f);
-  t.r4_lo = r4 * (1.0f - 0x1p-18f);
-  t.r4_hi = r4 * (1.0f + 0x1p-18f);
+  t.r6_lo = r6 * (1.0f - F46_BRACKET);
+  t.r6_hi = r6 * (1.0f + F46_BRACKET);
+  t.r4_lo = r4 * (1.0f - F46_BRACKET);
+  t.r4_hi = r4 * (1.0f + F46_BRACKET);
   return t;
 }
 
-// Block-scale code for target m with an exact tie fix.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Block-scale code for target m.  The two bracketing quotients give the same
+// E4M3 code unless bmax/(alpha*m) lies within 2^-17 of the E4M3 tie T between
+// them; then sign(alpha*T*m - bmax) decides exactly (T*m has <= 7
+// significant bits, the fma rounds once) and an exact tie goes to the even code.
 __device__ __forceinline__ uint32_t block_scale_code(float bmax, float alpha, float m, float r_lo,
                                                      float r_hi) {
   const uint32_t pr = cvt_e4m3x2(bmax * r_hi, bmax * r_lo);
   uint32_t sc = pr & 0xFF;
   const uint32_t sh = pr >> 8;
-  if (sh != sc) {
-    // bmax/(alpha*m) lies within 2^-17 of the E4M3 tie T between sc and sh:
-    // sign(alpha*T*m - bmax) is exact (T*m has <= 7 significant bits).
+  if (__builtin_expect(sh != sc, 0)) {
     const float T = 0.5f * (e4m3_to_f32(sc) + e4m3_to_f32(sh));
     const float s = fmaf(alpha, T * m, -bmax);
     sc = s > 0.f ? sc : (s < 0.f ? sh : ((sc & 1) ? sh : sc));
@@ -314,15 +326,37 @@ __device__ __forceinline__ uint32_t block_scale_code(float bmax, float alpha, fl
   return sc;
 }
 
+// 4 * (FP4 tie above magnitude code m), m = 0..6: 0.25 .75 1.25 1.75 2.5 3.5 5
+__device__ __forceinline__ float fp4_tie_above(uint32_t m) {
+  return (float)(__byte_perm(0x07050301u, 0x00140E0Au, m) & 0xFFu) * 0.25f;
+}
+
+// Resolve the flagged nibbles of one 8-code word exactly: code(q_lo) = m and
+// the true quotient is within 2^-16 of the tie t above m, so the true code is
+// m or m+1: sign(alpha*t*delta - |x|) decides (t*delta exact in f32), an exact
+// tie goes to the even code.  base = index of the word's first element.
+template <class Load>
+__device__ __forceinline__ uint32_t fix_word(uint32_t w, uint32_t dmask, int base, float alpha,
+                                             float delta, const Load& load) {
+  while (dmask) {
+    const int sh = (__ffs(dmask) - 1) & ~3;
+    const uint32_t m = (w >> sh) & 7u;
+    const float s = fmaf(alpha, fp4_tie_above(m) * delta, -fabsf(load(base + (sh >> 2))));
+    const uint32_t inc = (s < 0.f) | ((s == 0.f) & (m & 1u));
+    w += inc << sh;
+    dmask &= ~(0xFu << sh);
+  }
+  return w;
+}
+
 // FP4 codes of one block for decoded scale delta, with exact tie fixes.
 // `load` re-reads element i (rare path only).
 template <class Load>
 __device__ __forceinline__ uint64_t block_codes(const float2 (&x)[8], float alpha, float delta,
                                                 const Load& load) {
-  const float D = alpha * delta;
-  const float rD = __frcp_rn(D);
-  const float rlo = rD * (1.0f - 0x1p-18f);
-  const float rhi = rD * (1.0f + 0x1p-18f);
+  const float rD = rcp_approx(alpha * delta);
+  const float rlo = rD * (1.0f - F46_BRACKET);
+  const float rhi = rD * (1.0f + F46_BRACKET);
   const float2 rl2 = make_float2(rlo, rlo), rh2 = make_float2(rhi, rhi);
   float2 ql[8], qh[8];
 #pragma unroll
@@ -330,25 +364,15 @@ __device__ __forceinline__ uint64_t block_codes(const float2 (&x)[8], float alph
     ql[p] = __fmul2_rn(x[p], rl2);
     qh[p] = __fmul2_rn(x[p], rh2);
   }
-  const uint32_t l0 = cvt_e2m1x8(ql[0], ql[1], ql[2], ql[3]);
-  const uint32_t l1 = cvt_e2m1x8(ql[4], ql[5], ql[6], ql[7]);
-  const uint32_t h0 = cvt_e2m1x8(qh[0], qh[1], qh[2], qh[3]);
-  const uint32_t h1 = cvt_e2m1x8(qh[4], qh[5], qh[6], qh[7]);
-  uint64_t lo = ((uint64_t)l1 << 32) | l0;
-  const uint64_t hi = ((uint64_t)h1 << 32) | h0;
-  uint64_t diff = lo ^ hi;
-  while (diff) {
-    const int i = (__ffsll((long long)diff) - 1) >> 2;
-    const uint32_t clo = (uint32_t)(lo >> (4 * i)) & 15u;
-    const uint32_t chi = (uint32_t)(hi >> (4 * i)) & 15u;
-    const uint32_t mlo = clo & 7u, mhi = chi & 7u;
-    const float t = 0.5f * (fp4_mag_f32(mlo) + fp4_mag_f32(mhi));
-    const float s = fmaf(alpha, t * delta, -fabsf(load(i)));
-    const uint32_t c = s > 0.f ? clo : (s < 0.f ? chi : ((mlo & 1u) ? chi : clo));
-    lo = (lo & ~(0xFull << (4 * i))) | ((uint64_t)c << (4 * i));
-    diff &= ~(0xFull << (4 * i));
+  uint32_t l0 = cvt_e2m1x8(ql[0], ql[1], ql[2], ql[3]);
+  uint32_t l1 = cvt_e2m1x8(ql[4], ql[5], ql[6], ql[7]);
+  const uint32_t d0 = l0 ^ cvt_e2m1x8(qh[0], qh[1], qh[2], qh[3]);
+  const uint32_t d1 = l1 ^ cvt_e2m1x8(qh[4], qh[5], qh[6], qh[7]);
+  if (__builtin_expect((d0 | d1) != 0, 0)) {
+    l0 = fix_word(l0, d0, 0, alpha, delta, load);
+    l1 = fix_word(l1, d1, 8, alpha, delta, load);
   }
-  return lo;
+  return ((uint64_t)l1 << 32) | l0;
 }
 
 // f32 squared-error sum of one candidate: sum_i (v_i*delta*alpha - x_i)^2.
@@ -374,6 +398,18 @@ __device__ __forceinline__ float block_sq_err(const float2 (&x)[8], uint64_t cod
     acc = __ffma2_rn(d, d, acc);
   }
   return acc.x + acc.y;
+}
+
+// Ambiguous f32 comparison: decide S4 < S6 exactly in float64 (rare).
+template <class Load>
+__device__ __noinline__ uint32_t decide_exact(uint64_t c6, uint64_t c4, double alpha, double d6,
+                                              double d4, Load load) {
+  double xd[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) xd[i] = (double)load(i);
+  const double e6 = exact_sq_sum(xd, c6, alpha, d6);
+  const double e4 = exact_sq_sum(xd, c4, alpha, d4);
+  return e4 < e6;
 }
 
 // Quantize one block on the fast path.  Returns false when the block must take
@@ -415,22 +451,12 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
     const uint64_t c4 = block_codes(x, alpha, d4, load);
     const float s6 = block_sq_err(x, c6, alpha, d6);
     const float s4 = block_sq_err(x, c4, alpha, d4);
-    bool k;
-    if (s6 == 0.f && s4 == 0.f) {
-      k = false;  // both sums exactly zero in the reference too: tie -> 6
-    } else {
-      const float tol = (s4 + s6) * 0x1p-18f + 0x1p-140f;
-      if (fabsf(s6 - s4) > tol) {
-        k = s4 < s6;
-      } else {
-        double xd[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) xd[i] = (double)load(i);
-        const double e6 = exact_sq_sum(xd, c6, tc.alpha_d, (double)d6);
-        const double e4 = exact_sq_sum(xd, c4, tc.alpha_d, (double)d4);
-        k = e4 < e6;
-      }
-    }
+    // |S_f32 - S| <= 11 * 2^-24 * S (+ 2^-144 absolute for subnormal terms);
+    // both exactly zero means both reference sums are zero too (tie -> 6).
+    uint32_t k = s4 < s6;
+    const float tol = (s4 + s6) * 0x1p-18f + 0x1p-140f;
+    if (__builtin_expect(fabsf(s6 - s4) <= tol && (s6 != 0.f || s4 != 0.f), 0))
+      k = decide_exact(c6, c4, tc.alpha_d, (double)d6, (double)d4, load);
     out.codes = k ? c4 : c6;
     out.sc = k ? sc4 : sc6;
     out.pick4 = k;

@@ -28,7 +28,6 @@ using namespace f46;
 
 namespace {
 
-constexpr int kQThreads = 128;  // one thread per tile row
 constexpr int kStages = 3;
 
 int g_num_sms = 0;
@@ -112,150 +111,157 @@ __device__ __forceinline__ void prologue_flags(const QParams& p, double alpha) {
   }
 }
 
-// Re-read element i of the thread's block from the swizzled smem tile.
+// Re-read element i of the thread's block from the swizzled smem tile
+// (warp tile: 32 rows x 128 B per box, TMA SWIZZLE_128B).
 template <int DT>
 struct TileLoad {
-  const uint8_t* tile;
-  int r, kb;
+  const uint8_t* row;  // start of this thread's 128-byte row in box 0
+  int r7, kb;          // r & 7, block index within the 64-column tile
   __device__ __forceinline__ float operator()(int i) const {
     if constexpr (DT == DT_BF16) {
       const int chunk = 2 * kb + (i >> 3);
-      const uint8_t* q = tile + r * 128 + ((chunk ^ (r & 7)) << 4) + (i & 7) * 2;
-      return __uint_as_float((uint32_t)(*reinterpret_cast<const uint16_t*>(q)) << 16);
+      return __uint_as_float(
+          (uint32_t)(*reinterpret_cast<const uint16_t*>(row + ((chunk ^ r7) << 4) + (i & 7) * 2))
+          << 16);
     } else {
       const int chunk = (kb & 1) * 4 + (i >> 2);
-      const uint8_t* q =
-          tile + (kb >> 1) * 16384 + r * 128 + ((chunk ^ (r & 7)) << 4) + (i & 3) * 4;
-      return *reinterpret_cast<const float*>(q);
+      return *reinterpret_cast<const float*>(row + (kb >> 1) * 4096 + ((chunk ^ r7) << 4) +
+                                             (i & 3) * 4);
     }
   }
 };
 
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 template <int DT>
-__device__ __forceinline__ void load_tile_block(const uint8_t* tile, int r, int kb, float2 (&x)[8],
-                                                float& bmax, bool& nonfinite) {
+__device__ __forceinline__ void load_tile_block(const uint8_t* row, int r7, int kb, float2 (&x)[8],
+                                                float& bmax) {
   if constexpr (DT == DT_BF16) {
-    const uint4 a =
-        *reinterpret_cast<const uint4*>(tile + r * 128 + (((2 * kb) ^ (r & 7)) << 4));
-    const uint4 b =
-        *reinterpret_cast<const uint4*>(tile + r * 128 + (((2 * kb + 1) ^ (r & 7)) << 4));
+    const uint4 a = *reinterpret_cast<const uint4*>(row + (((2 * kb) ^ r7) << 4));
+    const uint4 b = *reinterpret_cast<const uint4*>(row + (((2 * kb + 1) ^ r7) << 4));
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    uint32_t m = 0;
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
+    for (int p = 0; p < 8; ++p)
       x[p] = make_float2(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u));
-      m = __vmaxu2(m, w[p] & 0x7FFF7FFFu);
-    }
-    const uint32_t mb = max(m & 0xFFFFu, m >> 16);
-    nonfinite |= (mb >= 0x7F80u);
-    bmax = __uint_as_float(mb << 16);
   } else {
-    const uint8_t* base = tile + (kb >> 1) * 16384 + r * 128;
-    uint32_t m = 0;
+    const uint8_t* base = row + (kb >> 1) * 4096;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int chunk = (kb & 1) * 4 + c;
-      const float4 v = *reinterpret_cast<const float4*>(base + ((chunk ^ (r & 7)) << 4));
+      const float4 v = *reinterpret_cast<const float4*>(base + ((chunk ^ r7) << 4));
       x[2 * c] = make_float2(v.x, v.y);
       x[2 * c + 1] = make_float2(v.z, v.w);
-      m = max(m, __float_as_uint(v.x) & 0x7FFFFFFFu);
-      m = max(m, __float_as_uint(v.y) & 0x7FFFFFFFu);
-      m = max(m, __float_as_uint(v.z) & 0x7FFFFFFFu);
-      m = max(m, __float_as_uint(v.w) & 0x7FFFFFFFu);
     }
-    nonfinite |= (m >= 0x7F800000u);
-    bmax = __uint_as_float(m);
   }
+  // NaN-propagating max: a NaN (or inf) block fails the fast path's range
+  // guard and is flagged on the exact path.
+  float m0 = fmax_nan(fabsf(x[0].x), fabsf(x[0].y)), m1 = fmax_nan(fabsf(x[1].x), fabsf(x[1].y));
+#pragma unroll
+  for (int p = 2; p < 8; p += 2) {
+    m0 = fmax_nan(m0, fmax_nan(fabsf(x[p].x), fabsf(x[p].y)));
+    m1 = fmax_nan(m1, fmax_nan(fabsf(x[p + 1].x), fabsf(x[p + 1].y)));
+  }
+  bmax = fmax_nan(m0, m1);
 }
 
 // ---------------------------------------------------------------------------
 // K2: TMA-pipelined quantize (cols % 64 == 0)
+//
+// Each warp is an independent pipeline: it owns kStages shared-memory stages
+// of one "warp tile" (32 rows x 64 columns; 4 KB of bf16, 8 KB of f32) and
+// its own mbarriers; lane 0 issues the TMA for a stage as soon as the warp has
+// consumed it.  Lane r quantizes row r of the tile: four 16-element blocks,
+// 32 B of packed codes and 4 scale bytes (one u32 of the tcgen05 128x4 layout).
 // ---------------------------------------------------------------------------
+constexpr int kWarps = 4;
+
 template <int DT, int MODE>
-__global__ void __launch_bounds__(kQThreads) quant_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                             QParams p) {
-  constexpr int kTileBytes = (DT == DT_BF16) ? 16384 : 32768;
+__global__ void __launch_bounds__(kWarps * 32) quant_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                               QParams p) {
+  constexpr int kBox = 4096;                              // 32 rows x 128 B
+  constexpr int kTileBytes = (DT == DT_BF16) ? kBox : 2 * kBox;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
 
-  const int tid = threadIdx.x;
-  const int64_t n_ct = p.cols >> 6;
-  const int64_t n_rt = (p.rows + 127) >> 7;
-  const int64_t total = n_ct * n_rt;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n_ct = (uint32_t)(p.cols >> 6);
+  const uint32_t n_rg = (uint32_t)((p.rows + 31) >> 5);  // 32-row groups holding data
+  const uint32_t total = n_ct * n_rg;
   const int64_t nb = p.cols >> 4;
+  const uint32_t gw = blockIdx.x * kWarps + warp, G = gridDim.x * kWarps;
 
   const double alpha_d = resolve_alpha(p);
   prologue_flags(p, alpha_d);
   const TensorConsts tc = make_consts(alpha_d, p.rule, DT);
 
-  if (tid == 0) {
+  uint8_t* wsm = smem + warp * (kStages * kTileBytes);
+  uint64_t* wb = bars[warp];
+  if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(&wb[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  __syncwarp();
 
-  auto issue = [&](int s, int64_t t) {
-    const int64_t rt = t / n_ct, ct = t - rt * n_ct;
-    uint8_t* dst = smem + s * kTileBytes;
-    mbar_expect_tx(&bars[s], kTileBytes);
-    if constexpr (DT == DT_BF16) {
-      tma_load_2d(dst, &tmap, &bars[s], (int)(ct * 64), (int)(rt * 128));
-    } else {
-      tma_load_2d(dst, &tmap, &bars[s], (int)(ct * 64), (int)(rt * 128));
-      tma_load_2d(dst + 16384, &tmap, &bars[s], (int)(ct * 64 + 32), (int)(rt * 128));
-    }
+  auto issue = [&](int s, uint32_t t) {
+    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
+    uint8_t* dst = wsm + s * kTileBytes;
+    mbar_expect_tx(&wb[s], kTileBytes);
+    tma_load_2d(dst, &tmap, &wb[s], (int)(ct * 64), (int)(rg * 32));
+    if constexpr (DT != DT_BF16) tma_load_2d(dst + kBox, &tmap, &wb[s], (int)(ct * 64 + 32), (int)(rg * 32));
   };
-
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
-      if (t < total) issue(s, t);
-    }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      if (gw + s * G < total) issue(s, gw + s * G);
   }
 
   bool nonfinite = false;
-  int it = 0;
-  for (int64_t t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+  uint32_t it = 0;
+  for (uint32_t t = gw; t < total; t += G, ++it) {
     const int s = it % kStages;
-    const uint32_t parity = (uint32_t)(it / kStages) & 1u;
-    mbar_wait(&bars[s], parity);
-    const uint8_t* tile = smem + s * kTileBytes;
-    const int64_t rt = t / n_ct, ct = t - rt * n_ct;
-    const int64_t grow = rt * 128 + tid;
-    const bool live = grow < p.rows;
+    mbar_wait(&wb[s], (it / kStages) & 1u);
+    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
+    const int64_t grow = (int64_t)rg * 32 + lane;
+    const uint8_t* row = wsm + s * kTileBytes + lane * 128;
+    const int r7 = lane & 7;
 
     uint64_t codes[4];
     uint32_t scw = 0, pkw = 0;
-#pragma unroll
+#pragma unroll 1
     for (int kb = 0; kb < 4; ++kb) {
       float2 x[8];
       float bmax;
-      load_tile_block<DT>(tile, tid, kb, x, bmax, nonfinite);
-      const TileLoad<DT> ld{tile, tid, kb};
+      load_tile_block<DT>(row, r7, kb, x, bmax);
+      const TileLoad<DT> ld{row, r7, kb};
       BlockOut o;
       bool ok = false;
       if (!tc.force_exact) ok = fast_block<MODE>(x, bmax, tc, ld, o);
-      if (!ok) {
+      if (__builtin_expect(!ok, 0)) {
         double xd[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) xd[i] = (double)ld(i);
+        for (int i = 0; i < 16; ++i) {
+          xd[i] = (double)ld(i);
+          nonfinite |= !(fabs(xd[i]) <= 3.4028234663852886e38);
+        }
         exact_block(xd, alpha_d, MODE, p.rule, &o);
       }
       codes[kb] = o.codes;
       scw |= o.sc << (8 * kb);
       pkw |= o.pick4 << (8 * kb);
     }
-    __syncthreads();  // every thread is done with stage s
-    if (tid == 0) {
-      const int64_t tn = t + (int64_t)kStages * gridDim.x;
-      if (tn < total) issue(s, tn);
-    }
+    __syncwarp();
+    if (lane == 0 && t + kStages * G < total) issue(s, t + kStages * G);
 
-    // tcgen05 scale tile: this CTA tile's 128x4 scales are one 512-byte chunk.
-    *reinterpret_cast<uint32_t*>(p.scales_tc + (rt * n_ct + ct) * 512 + (tid & 31) * 16 +
-                                 (tid >> 5) * 4) = live ? scw : 0u;
+    const bool live = grow < p.rows;
+    const int64_t rt = grow >> 7;
+    *reinterpret_cast<uint32_t*>(p.scales_tc + (rt * n_ct + ct) * 512 + (lane & 31) * 16 +
+                                 ((grow & 127) >> 5) * 4) = live ? scw : 0u;
     if (live) {
       uint4* dst = reinterpret_cast<uint4*>(p.codes + grow * (p.cols >> 1) + ct * 32);
       dst[0] = make_uint4((uint32_t)codes[0], (uint32_t)(codes[0] >> 32), (uint32_t)codes[1],
@@ -265,6 +271,14 @@ __global__ void __launch_bounds__(kQThreads) quant_tma_kernel(const __grid_const
       if (p.scales_rm) *reinterpret_cast<uint32_t*>(p.scales_rm + grow * nb + ct * 4) = scw;
       if (p.pick4) *reinterpret_cast<uint32_t*>(p.pick4 + grow * nb + ct * 4) = pkw;
     }
+  }
+  // 32-row groups that only exist as padding of the last 128-row scale tile
+  const uint32_t n_rg_pad = (uint32_t)(((p.rows + 127) >> 7) << 2);
+  for (uint32_t t = n_rg * n_ct + gw; t < n_rg_pad * n_ct; t += G) {
+    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
+    const int64_t grow = (int64_t)rg * 32 + lane;
+    *reinterpret_cast<uint32_t*>(p.scales_tc + ((grow >> 7) * n_ct + ct) * 512 + lane * 16 +
+                                 ((grow & 127) >> 5) * 4) = 0u;
   }
   if (nonfinite && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
 }
@@ -554,28 +568,29 @@ int launch_quant_tma(const QParams& p, cudaStream_t s) {
   const int esz = DT == DT_BF16 ? 2 : 4;
   cuuint64_t dims[2] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows};
   cuuint64_t strides[1] = {(cuuint64_t)(p.cols * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 128};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(&map, DT == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, const_cast<void*>(p.x), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return F46_ERR_UNSUPPORTED;
-  constexpr int kTileBytes = (DT == DT_BF16) ? 16384 : 32768;
-  const int smem = kStages * kTileBytes + 1024;
+  constexpr int kTileBytes = (DT == DT_BF16) ? 4096 : 8192;
+  const int smem = kWarps * kStages * kTileBytes + 1024;
   static bool configured = false;
   static int ctas_per_sm = 1;
   if (!configured) {
     cudaFuncSetAttribute(quant_tma_kernel<DT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_tma_kernel<DT, MODE>,
-                                                  kQThreads, smem);
+                                                  kWarps * 32, smem);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
     configured = true;
   }
-  const int64_t total = (p.cols >> 6) * ((p.rows + 127) >> 7);
-  const int64_t grid = total < (int64_t)num_sms() * ctas_per_sm ? total : (int64_t)num_sms() * ctas_per_sm;
-  quant_tma_kernel<DT, MODE><<<(unsigned)grid, kQThreads, smem, s>>>(map, p);
+  const int64_t wtiles = (p.cols >> 6) * ((p.rows + 127) >> 7) * 4;
+  int64_t grid = (wtiles + kWarps - 1) / kWarps;
+  if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
+  quant_tma_kernel<DT, MODE><<<(unsigned)grid, kWarps * 32, smem, s>>>(map, p);
   return launch_status();
 }
 
