@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfouroversix.so")
+LIB_PATH = os.environ.get("F46_LIB_PATH") or os.path.join(_HERE, "libfouroversix.so")
 
 # constants mirrored from include/fouroversix.h
 F46_OK = 0

@@ -63,22 +63,18 @@ __device__ __forceinline__ uint32_t cvt_e2m1x8(float2 a, float2 b, float2 c, flo
   return r;
 }
 
-// Byte k of w (two E2M1 codes) -> f16x2 (exact).
+// Byte k of w (two E2M1 codes) -> f16x2 (exact); the low nibble (even
+// element) lands in the low half.  The byte is handed over in a 16-bit
+// register split with mov.b16 (as cuda_fp4.hpp does): a 4-way .b8 vector
+// split of a 32-bit register mis-selected bytes under ptxas 12.9.
 template <int K>
 __device__ __forceinline__ __half2 e2m1x2_to_h2(uint32_t w) {
   uint32_t r;
-  if constexpr (K == 0)
-    asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\tmov.b32 {b0, b1, b2, b3}, %1;\n\t"
-        "cvt.rn.f16x2.e2m1x2 %0, b0;\n\t}" : "=r"(r) : "r"(w));
-  else if constexpr (K == 1)
-    asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\tmov.b32 {b0, b1, b2, b3}, %1;\n\t"
-        "cvt.rn.f16x2.e2m1x2 %0, b1;\n\t}" : "=r"(r) : "r"(w));
-  else if constexpr (K == 2)
-    asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\tmov.b32 {b0, b1, b2, b3}, %1;\n\t"
-        "cvt.rn.f16x2.e2m1x2 %0, b2;\n\t}" : "=r"(r) : "r"(w));
-  else
-    asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\tmov.b32 {b0, b1, b2, b3}, %1;\n\t"
-        "cvt.rn.f16x2.e2m1x2 %0, b3;\n\t}" : "=r"(r) : "r"(w));
+  const uint16_t b = (uint16_t)((w >> (8 * K)) & 0xFFu);
+  asm("{\n\t.reg .b8 lo, hi;\n\tmov.b16 {lo, hi}, %1;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %0, lo;\n\t}"
+      : "=r"(r)
+      : "h"(b));
   return *reinterpret_cast<__half2*>(&r);
 }
 
@@ -234,8 +230,8 @@ struct BlockOut {
 // Full exact block (adaptive.py:60-101 / blockquant.py:334-360 for one block).
 // Pad positions must be passed as 0.0 and are zeroed in the returned codes by
 // the caller's tail handling.
-__device__ __noinline__ void exact_block(const double* xin, double alpha, int mode, int rule,
-                                         BlockOut* out) {
+__device__ __forceinline__ void exact_block_inl(const double* xin, double alpha, int mode, int rule,
+                                                BlockOut* out) {
   double x[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = xin[i];
@@ -253,6 +249,11 @@ __device__ __noinline__ void exact_block(const double* xin, double alpha, int mo
     out->sc = p6.sc;
     out->pick4 = (mode == FIXED4);
   }
+}
+
+__device__ __noinline__ void exact_block(const double* xin, double alpha, int mode, int rule,
+                                         BlockOut* out) {
+  exact_block_inl(xin, alpha, mode, rule, out);
 }
 
 // Exact float64 squared-error sum of one candidate whose codes are known
@@ -280,15 +281,43 @@ struct TensorConsts {
   float alpha;
   float r6_lo, r6_hi, r4_lo, r4_hi;  // bracketing 1/(alpha*m)
   int force_exact;                   // alpha outside the fast path's range
+  // Rounding direction of bracket-flagged FP4 codes (see tie_direction()):
+  // -1 keep the lower code, +1 take the upper code, 0 ties-to-even,
+  // 2 unknown -> exact per-element test.
+  int tdir;
 };
 
-// Relative half-width of the brackets.  Every f32 quantity below carries at
-// most ~2^-21.7 relative error (one approximate reciprocal, <= 1 ulp, plus
+// For BF16 input whose alpha was computed from amax A (no override), every
+// element whose quotient x/(alpha*Delta) lies within 2^-19.5 of an FP4 tie t
+// is an exact tie of the *unrounded* scale beta = A/mcap:
+//   q_beta = |x|*mcap/(A*Delta) = (4*X*M*2^k)/(T*Y*S)  with X, Y (8-bit bf16
+//   significands), M the odd part of mcap (<= 21), S (E4M3 significand, <= 15),
+//   T = 4t <= 20, so q_beta != t implies |q_beta - t| >= t * 2^-16.3, while
+//   |q/q_beta - 1| = |beta/alpha - 1| <= 2^-24.
+// Hence q = t*beta/alpha and the reference's exact-real rounding goes down if
+// alpha > beta, up if alpha < beta and to even if alpha == beta -- one sign for
+// the whole tensor, decided exactly here (alpha*mcap has <= 29 bits).
+__device__ __forceinline__ int tie_direction(double alpha, double amax, double mcap, int dtype,
+                                             bool overridden) {
+  if (dtype != DT_BF16 || overridden || !(amax > 0.0)) return 2;
+  const double d = alpha * mcap - amax;  // exact
+  return d > 0.0 ? -1 : (d < 0.0 ? 1 : 0);
+}
+
+// Relative half-width of the scale brackets.  Every f32 quantity below carries
+// at most 2^-21.9 relative error (one approximate reciprocal, <= 1 ulp, plus
 // three RN roundings), so x*r_lo < x/(alpha*m) < x*r_hi strictly.
 #define F46_BRACKET 0x1p-17f
+// Codes are computed from q = x * rD * (1 - 11*2^-24), a strict lower bound of
+// the true quotient x/(alpha*Delta) (and within 2^-19.9 of it); the winner's
+// codes are checked against q * (1 + 11*2^-23), a strict upper bound.
+#define F46_QLO (1.0f - 11.0f * 0x1p-24f) /* 1 - 2^-20.54, exact in f32 */
+#define F46_QHI_OVER_QLO (1.0f + 11.0f * 0x1p-23f) /* exact in f32 */
 
-__device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, int dtype) {
+__device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, int dtype,
+                                                   int tdir = 2) {
   TensorConsts t;
+  t.tdir = tdir;
   t.alpha_d = alpha_d;
   t.alpha = (float)alpha_d;
   const bool f32_exact = ((double)t.alpha == alpha_d);
@@ -306,6 +335,12 @@ __device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, in
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
 
@@ -332,7 +367,7 @@ __device__ __forceinline__ float fp4_tie_above(uint32_t m) {
 }
 
 // Resolve the flagged nibbles of one 8-code word exactly: code(q_lo) = m and
-// the true quotient is within 2^-16 of the tie t above m, so the true code is
+// the true quotient may lie at or above the tie t above m, so the true code is
 // m or m+1: sign(alpha*t*delta - |x|) decides (t*delta exact in f32), an exact
 // tie goes to the even code.  base = index of the word's first element.
 template <class Load>
@@ -349,71 +384,85 @@ __device__ __forceinline__ uint32_t fix_word(uint32_t w, uint32_t dmask, int bas
   return w;
 }
 
-// FP4 codes of one block for decoded scale delta, with exact tie fixes.
-// `load` re-reads element i (rare path only).
-template <class Load>
-__device__ __forceinline__ uint64_t block_codes(const float2 (&x)[8], float alpha, float delta,
-                                                const Load& load) {
-  const float rD = rcp_approx(alpha * delta);
-  const float rlo = rD * (1.0f - F46_BRACKET);
-  const float rhi = rD * (1.0f + F46_BRACKET);
-  const float2 rl2 = make_float2(rlo, rlo), rh2 = make_float2(rhi, rhi);
-  float2 ql[8], qh[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    ql[p] = __fmul2_rn(x[p], rl2);
-    qh[p] = __fmul2_rn(x[p], rh2);
-  }
-  uint32_t l0 = cvt_e2m1x8(ql[0], ql[1], ql[2], ql[3]);
-  uint32_t l1 = cvt_e2m1x8(ql[4], ql[5], ql[6], ql[7]);
-  const uint32_t d0 = l0 ^ cvt_e2m1x8(qh[0], qh[1], qh[2], qh[3]);
-  const uint32_t d1 = l1 ^ cvt_e2m1x8(qh[4], qh[5], qh[6], qh[7]);
-  if (__builtin_expect((d0 | d1) != 0, 0)) {
-    l0 = fix_word(l0, d0, 0, alpha, delta, load);
-    l1 = fix_word(l1, d1, 8, alpha, delta, load);
-  }
-  return ((uint64_t)l1 << 32) | l0;
+// r = v - q in one FHADD (f16 half + f32, single rounding), r^2 accumulated.
+__device__ __forceinline__ float fhadd(__half v, float negq) {
+  float r;
+  asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(r) : "h"(__half_as_ushort(v)), "f"(negq));
+  return r;
 }
 
-// f32 squared-error sum of one candidate: sum_i (v_i*delta*alpha - x_i)^2.
-__device__ __forceinline__ float block_sq_err(const float2 (&x)[8], uint64_t codes, float alpha,
-                                              float delta) {
-  const __half2 dh = __float2half2_rn(delta);
-  const float2 a2 = make_float2(alpha, alpha);
-  float2 acc = make_float2(0.f, 0.f);
-  const uint32_t w0 = (uint32_t)codes, w1 = (uint32_t)(codes >> 32);
+// One candidate on the fast path: codes of the lower-bound quotients and the
+// quotient-space squared error sum  sum_i (v_i - q_i)^2  (q_i ~ x_i/(alpha*Delta)).
+struct Cand {
+  uint32_t w0, w1;  // codes (elements 0-7, 8-15)
+  float rq;         // the lower-bound reciprocal used
+  float sq;         // quotient-space error sum
+};
+
+__device__ __forceinline__ void cand_eval(const float2 (&x)[8], float D, Cand& c) {
+  c.rq = rcp_approx(D) * F46_QLO;
+  const float2 r2 = make_float2(c.rq, c.rq);
+  float2 q[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
+  c.w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  c.w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]);
   __half2 v[8];
-  v[0] = e2m1x2_to_h2<0>(w0);
-  v[1] = e2m1x2_to_h2<1>(w0);
-  v[2] = e2m1x2_to_h2<2>(w0);
-  v[3] = e2m1x2_to_h2<3>(w0);
-  v[4] = e2m1x2_to_h2<0>(w1);
-  v[5] = e2m1x2_to_h2<1>(w1);
-  v[6] = e2m1x2_to_h2<2>(w1);
-  v[7] = e2m1x2_to_h2<3>(w1);
+  v[0] = e2m1x2_to_h2<0>(c.w0);
+  v[1] = e2m1x2_to_h2<1>(c.w0);
+  v[2] = e2m1x2_to_h2<2>(c.w0);
+  v[3] = e2m1x2_to_h2<3>(c.w0);
+  v[4] = e2m1x2_to_h2<0>(c.w1);
+  v[5] = e2m1x2_to_h2<1>(c.w1);
+  v[6] = e2m1x2_to_h2<2>(c.w1);
+  v[7] = e2m1x2_to_h2<3>(c.w1);
+  float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
-    const float2 vd = __half22float2(__hmul2(v[p], dh));  // exact
-    const float2 d = __ffma2_rn(vd, a2, make_float2(-x[p].x, -x[p].y));
-    acc = __ffma2_rn(d, d, acc);
+    const float2 r = make_float2(fhadd(__low2half(v[p]), -q[p].x), fhadd(__high2half(v[p]), -q[p].y));
+    acc = __ffma2_rn(r, r, acc);
   }
-  return acc.x + acc.y;
+  c.sq = acc.x + acc.y;
 }
 
-// Ambiguous f32 comparison: decide S4 < S6 exactly in float64 (rare).
+// Exact codes for the stored candidate.  w0/w1 are the codes of the strict
+// lower-bound quotient q; the codes of the strict upper bound q*QHI/QLO agree
+// with them except at nibbles whose bracket straddles an FP4 tie, where the
+// true code is one of the two.  With a known tensor-wide tie direction the
+// choice is a word select; otherwise each flagged nibble gets the exact test.
 template <class Load>
-__device__ __noinline__ uint32_t decide_exact(uint64_t c6, uint64_t c4, double alpha, double d6,
-                                              double d4, Load load) {
-  double xd[16];
+__device__ __forceinline__ uint64_t exact_codes(const float2 (&x)[8], uint32_t w0, uint32_t w1,
+                                                float rq, float alpha, float delta, int tdir,
+                                                const Load& load) {
+  if (tdir < 0) return ((uint64_t)w1 << 32) | w0;
+  const float rh = rq * F46_QHI_OVER_QLO;
+  const float2 rh2 = make_float2(rh, rh);
+  float2 qh[8];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) xd[i] = (double)load(i);
-  const double e6 = exact_sq_sum(xd, c6, alpha, d6);
-  const double e4 = exact_sq_sum(xd, c4, alpha, d4);
-  return e4 < e6;
+  for (int p = 0; p < 8; ++p) qh[p] = __fmul2_rn(x[p], rh2);
+  const uint32_t h0 = cvt_e2m1x8(qh[0], qh[1], qh[2], qh[3]);
+  const uint32_t h1 = cvt_e2m1x8(qh[4], qh[5], qh[6], qh[7]);
+  if (tdir == 1) return ((uint64_t)h1 << 32) | h0;
+  const uint32_t d0 = w0 ^ h0, d1 = w1 ^ h1;
+  if (tdir == 0) {
+    // exact ties: take the upper code where the lower one has an odd magnitude
+    auto even = [](uint32_t lo, uint32_t hi, uint32_t d) {
+      const uint32_t flag = (d | (d >> 1) | (d >> 2) | (d >> 3)) & 0x11111111u;
+      const uint32_t up = (flag & lo) * 0xFu;
+      return (lo & ~up) | (hi & up);
+    };
+    return ((uint64_t)even(w1, h1, d1) << 32) | even(w0, h0, d0);
+  }
+  if (__builtin_expect((d0 | d1) != 0, 0)) {
+    w0 = fix_word(w0, d0, 0, alpha, delta, load);
+    w1 = fix_word(w1, d1, 8, alpha, delta, load);
+  }
+  return ((uint64_t)w1 << 32) | w0;
 }
 
 // Quantize one block on the fast path.  Returns false when the block must take
-// the exact path (underflowed scale, or values outside the guarded range).
+// the exact path (underflowed scale, values outside the guarded range, or an
+// adaptive decision the certified f32 bound cannot settle).
 template <int MODE, class Load>
 __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, const TensorConsts& tc,
                                            const Load& load, BlockOut& out) {
@@ -438,7 +487,14 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
     const uint32_t sc = block_scale_code(bmax, alpha, m, MODE == FIXED6 ? tc.r6_lo : tc.r4_lo,
                                          MODE == FIXED6 ? tc.r6_hi : tc.r4_hi);
     if (sc == 0) return false;
-    out.codes = block_codes(x, alpha, e4m3_to_f32(sc), load);
+    const float delta = e4m3_to_f32(sc);
+    const float rq = rcp_approx(alpha * delta) * F46_QLO;
+    const float2 r2 = make_float2(rq, rq);
+    float2 q[8];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
+    out.codes = exact_codes(x, cvt_e2m1x8(q[0], q[1], q[2], q[3]), cvt_e2m1x8(q[4], q[5], q[6], q[7]),
+                            rq, alpha, delta, tc.tdir, load);
     out.sc = sc;
     out.pick4 = (MODE == FIXED4);
     return true;
@@ -447,17 +503,24 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
     const uint32_t sc4 = block_scale_code(bmax, alpha, 4.f, tc.r4_lo, tc.r4_hi);
     if (sc6 == 0 || sc4 == 0) return false;
     const float d6 = e4m3_to_f32(sc6), d4 = e4m3_to_f32(sc4);
-    const uint64_t c6 = block_codes(x, alpha, d6, load);
-    const uint64_t c4 = block_codes(x, alpha, d4, load);
-    const float s6 = block_sq_err(x, c6, alpha, d6);
-    const float s4 = block_sq_err(x, c4, alpha, d4);
-    // |S_f32 - S| <= 11 * 2^-24 * S (+ 2^-144 absolute for subnormal terms);
-    // both exactly zero means both reference sums are zero too (tie -> 6).
-    uint32_t k = s4 < s6;
-    const float tol = (s4 + s6) * 0x1p-18f + 0x1p-140f;
-    if (__builtin_expect(fabsf(s6 - s4) <= tol && (s6 != 0.f || s4 != 0.f), 0))
-      k = decide_exact(c6, c4, tc.alpha_d, (double)d6, (double)d4, load);
-    out.codes = k ? c4 : c6;
+    const float D6 = alpha * d6, D4 = alpha * d4;
+    Cand c6, c4;
+    cand_eval(x, D6, c6);
+    cand_eval(x, D4, c4);
+    // x-space sums S_m = D_m^2 * sq_m.  Certified bound on |S_m(f32) - S_m(ref)|
+    // (DESIGN.md section "decision bound"): quotient error 2^-19.9 ->
+    // 2^-18.9 * sqrt(S_m * sum x^2) <= 2^-16.9 * bmax * sqrt(S_m); codes taken
+    // from the lower-bound quotient can differ from the exact ones only at
+    // near-ties, moving S_m by <= 2^-15.1 * S_m; f32 rounding <= 2^-20 * S_m;
+    // second-order quotient terms <= 2^-33.8 * bmax^2.
+    const float s6 = c6.sq * (D6 * D6), s4 = c4.sq * (D4 * D4);
+    const float tol = 0x1p-16f * bmax * (sqrt_approx(s6) + sqrt_approx(s4)) +
+                      0x1p-14f * (s6 + s4) + 0x1p-32f * (bmax * bmax) + 0x1p-140f;
+    if (__builtin_expect(fabsf(s6 - s4) <= tol, 0)) return false;  // exact path decides
+    const bool k = s4 < s6;
+    const float delta = k ? d4 : d6;
+    out.codes = exact_codes(x, k ? c4.w0 : c6.w0, k ? c4.w1 : c6.w1, k ? c4.rq : c6.rq, alpha,
+                            delta, tc.tdir, load);
     out.sc = k ? sc4 : sc6;
     out.pick4 = k;
     return true;

@@ -111,23 +111,34 @@ __device__ __forceinline__ void prologue_flags(const QParams& p, double alpha) {
   }
 }
 
-// Re-read element i of the thread's block from the swizzled smem tile
-// (warp tile: 32 rows x 128 B per box, TMA SWIZZLE_128B).
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+// Re-read element i of the thread's block from the shared-memory segment
+// (`blk` = shared-space address of the block's first element).
 template <int DT>
-struct TileLoad {
-  const uint8_t* row;  // start of this thread's 128-byte row in box 0
-  int r7, kb;          // r & 7, block index within the 64-column tile
+struct SegLoad {
+  uint32_t blk;
   __device__ __forceinline__ float operator()(int i) const {
-    if constexpr (DT == DT_BF16) {
-      const int chunk = 2 * kb + (i >> 3);
-      return __uint_as_float(
-          (uint32_t)(*reinterpret_cast<const uint16_t*>(row + ((chunk ^ r7) << 4) + (i & 7) * 2))
-          << 16);
-    } else {
-      const int chunk = (kb & 1) * 4 + (i >> 2);
-      return *reinterpret_cast<const float*>(row + (kb >> 1) * 4096 + ((chunk ^ r7) << 4) +
-                                             (i & 3) * 4);
-    }
+    if constexpr (DT == DT_BF16)
+      return __uint_as_float(lds_u16(blk + i * 2) << 16);
+    else
+      return lds_f32(blk + i * 4);
   }
 };
 
@@ -138,23 +149,20 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
 }
 
 template <int DT>
-__device__ __forceinline__ void load_tile_block(const uint8_t* row, int r7, int kb, float2 (&x)[8],
-                                                float& bmax) {
+__device__ __forceinline__ void load_block(uint32_t blk, float2 (&x)[8], float& bmax) {
   if constexpr (DT == DT_BF16) {
-    const uint4 a = *reinterpret_cast<const uint4*>(row + (((2 * kb) ^ r7) << 4));
-    const uint4 b = *reinterpret_cast<const uint4*>(row + (((2 * kb + 1) ^ r7) << 4));
+    const uint4 a = lds128(blk);
+    const uint4 b = lds128(blk + 16);
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
     for (int p = 0; p < 8; ++p)
       x[p] = make_float2(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u));
   } else {
-    const uint8_t* base = row + (kb >> 1) * 4096;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const int chunk = (kb & 1) * 4 + c;
-      const float4 v = *reinterpret_cast<const float4*>(base + ((chunk ^ r7) << 4));
-      x[2 * c] = make_float2(v.x, v.y);
-      x[2 * c + 1] = make_float2(v.z, v.w);
+      const uint4 v = lds128(blk + 16 * c);
+      x[2 * c] = make_float2(__uint_as_float(v.x), __uint_as_float(v.y));
+      x[2 * c + 1] = make_float2(__uint_as_float(v.z), __uint_as_float(v.w));
     }
   }
   // NaN-propagating max: a NaN (or inf) block fails the fast path's range
@@ -169,38 +177,106 @@ __device__ __forceinline__ void load_tile_block(const uint8_t* row, int r7, int 
 }
 
 // ---------------------------------------------------------------------------
-// K2: TMA-pipelined quantize (cols % 64 == 0)
+// K2: bulk-copy-pipelined quantize (cols % 16 == 0)
 //
-// Each warp is an independent pipeline: it owns kStages shared-memory stages
-// of one "warp tile" (32 rows x 64 columns; 4 KB of bf16, 8 KB of f32) and
-// its own mbarriers; lane 0 issues the TMA for a stage as soon as the warp has
-// consumed it.  Lane r quantizes row r of the tile: four 16-element blocks,
-// 32 B of packed codes and 4 scale bytes (one u32 of the tcgen05 128x4 layout).
+// Each warp is an independent pipeline over "segments": kSegElems contiguous
+// elements of one row (4 KB of bf16 / 8 KB of f32).  Lane 0 streams segments
+// into kStages shared-memory stages with 1-D bulk copies (cp.async.bulk,
+// mbarrier complete_tx); lane l then quantizes blocks l, l+32, l+64, l+96 of
+// the segment, so the warp's 8-byte code stores are fully coalesced (256 B per
+// instruction).  Blocks the fast path cannot certify are queued in a per-warp
+// shared list and recomputed exactly outside the hot loop.
 // ---------------------------------------------------------------------------
 constexpr int kWarps = 4;
+constexpr int kSegElems = 2048;
+#ifndef F46_KB_UNROLL
+#define F46_KB_UNROLL 1
+#endif
+constexpr int kKbUnroll = F46_KB_UNROLL;
+#ifndef F46_MINB
+#define F46_MINB 4
+#endif
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Exact f64 recomputation of one block, reading its 16 values from global
+// memory (used for the rare blocks the fast path defers).  Arguments by value:
+// taking the address of the kernel's parameter struct would force a copy to
+// local memory.
+struct ExactArgs {
+  const void* x;
+  uint8_t* codes;
+  uint8_t* scales_tc;
+  uint8_t* scales_rm;
+  uint8_t* pick4;
+  int64_t cols;
+  int mode, rule;
+};
+
+template <int DT>
+__device__ __forceinline__ void exact_block_global(ExactArgs a, double alpha, uint32_t blk,
+                                                   uint32_t kb4, uint32_t* nonfinite) {
+  const int64_t nb = (a.cols + 15) >> 4;
+  const int64_t row = blk / nb, kbg = blk - row * nb;
+  double xd[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int64_t c = kbg * 16 + i;
+    if (c >= a.cols)
+      xd[i] = 0.0;
+    else if constexpr (DT == DT_BF16)
+      xd[i] = (double)__uint_as_float(
+          (uint32_t)(reinterpret_cast<const uint16_t*>(a.x)[row * a.cols + c]) << 16);
+    else
+      xd[i] = (double)reinterpret_cast<const float*>(a.x)[row * a.cols + c];
+  }
+  bool nf = false;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) nf |= !(fabs(xd[i]) <= 3.4028234663852886e38);
+  if (nf && nonfinite) atomicOr(nonfinite, F46_FLAG_NONFINITE);
+  BlockOut o;
+  exact_block_inl(xd, alpha, a.mode, a.rule, &o);
+  *reinterpret_cast<uint64_t*>(a.codes + (row * nb + kbg) * 8) = o.codes;
+  a.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
+  if (a.scales_rm) a.scales_rm[row * nb + kbg] = (uint8_t)o.sc;
+  if (a.pick4) a.pick4[row * nb + kbg] = (uint8_t)o.pick4;
+}
+
+constexpr int kDefer = 256;  // deferred-block slots per warp (a segment defers <= 128)
 
 template <int DT, int MODE>
-__global__ void __launch_bounds__(kWarps * 32) quant_tma_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                               QParams p) {
-  constexpr int kBox = 4096;                              // 32 rows x 128 B
-  constexpr int kTileBytes = (DT == DT_BF16) ? kBox : 2 * kBox;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+__global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParams p) {
+  constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
+  constexpr int kTileBytes = kSegElems * kEsz;
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+  __shared__ uint32_t defer[kWarps][kDefer];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t n_ct = (uint32_t)(p.cols >> 6);
-  const uint32_t n_rg = (uint32_t)((p.rows + 31) >> 5);  // 32-row groups holding data
-  const uint32_t total = n_ct * n_rg;
-  const int64_t nb = p.cols >> 4;
+  const uint32_t cols = (uint32_t)p.cols;
+  const uint32_t nb = cols >> 4;
+  const uint32_t kb4 = (nb + 3) >> 2;
+  const uint32_t n_seg = (cols + kSegElems - 1) / kSegElems;
+  const uint32_t total = (uint32_t)p.rows * n_seg;
   const uint32_t gw = blockIdx.x * kWarps + warp, G = gridDim.x * kWarps;
 
   const double alpha_d = resolve_alpha(p);
   prologue_flags(p, alpha_d);
-  const TensorConsts tc = make_consts(alpha_d, p.rule, DT);
+  const bool overridden = p.alpha_override > 0.0;
+  const TensorConsts tc = make_consts(
+      alpha_d, p.rule, DT,
+      tie_direction(alpha_d, overridden ? 0.0 : *p.d_amax, p.mcap, DT, overridden));
+  const bool all_exact = tc.force_exact;
 
-  uint8_t* wsm = smem + warp * (kStages * kTileBytes);
+  const uint32_t wsm = smem_u32(smem) + warp * (kStages * kTileBytes);
   uint64_t* wb = bars[warp];
+  uint32_t* dl = defer[warp];
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(&wb[s], 1);
@@ -208,77 +284,117 @@ __global__ void __launch_bounds__(kWarps * 32) quant_tma_kernel(const __grid_con
   }
   __syncwarp();
 
-  auto issue = [&](int s, uint32_t t) {
-    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
-    uint8_t* dst = wsm + s * kTileBytes;
-    mbar_expect_tx(&wb[s], kTileBytes);
-    tma_load_2d(dst, &tmap, &wb[s], (int)(ct * 64), (int)(rg * 32));
-    if constexpr (DT != DT_BF16) tma_load_2d(dst + kBox, &tmap, &wb[s], (int)(ct * 64 + 32), (int)(rg * 32));
+  const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
+  auto issue = [&](int s, uint32_t row, uint32_t seg) {
+    const uint32_t c0 = seg * kSegElems;
+    const uint32_t n = min((uint32_t)kSegElems, cols - c0);
+    mbar_expect_tx(&wb[s], n * kEsz);
+    bulk_load(wsm + s * kTileBytes, xb + ((uint64_t)row * cols + c0) * kEsz, n * kEsz, &wb[s]);
   };
-  if (lane == 0) {
+  // (row, seg) of tile t, advanced by G = g_row * n_seg + g_seg without division
+  const uint32_t g_row = G / n_seg, g_seg = G - g_row * n_seg;
+  auto advance = [&](uint32_t& row, uint32_t& seg) {
+    row += g_row;
+    seg += g_seg;
+    if (seg >= n_seg) {
+      seg -= n_seg;
+      ++row;
+    }
+  };
+  uint32_t row = gw / n_seg, seg = gw - (gw / n_seg) * n_seg;  // tile being consumed
+  uint32_t irow = row, iseg = seg;                             // next tile to issue
+  uint32_t tnext = gw;
+  if (lane == 0 && !all_exact) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s)
-      if (gw + s * G < total) issue(s, gw + s * G);
+    for (int s = 0; s < kStages; ++s) {
+      if (tnext < total) issue(s, irow, iseg);
+      tnext += G;
+      advance(irow, iseg);
+    }
   }
 
   bool nonfinite = false;
-  uint32_t it = 0;
-  for (uint32_t t = gw; t < total; t += G, ++it) {
-    const int s = it % kStages;
-    mbar_wait(&wb[s], (it / kStages) & 1u);
-    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
-    const int64_t grow = (int64_t)rg * 32 + lane;
-    const uint8_t* row = wsm + s * kTileBytes + lane * 128;
-    const int r7 = lane & 7;
-
-    uint64_t codes[4];
-    uint32_t scw = 0, pkw = 0;
-#pragma unroll 1
-    for (int kb = 0; kb < 4; ++kb) {
-      float2 x[8];
-      float bmax;
-      load_tile_block<DT>(row, r7, kb, x, bmax);
-      const TileLoad<DT> ld{row, r7, kb};
-      BlockOut o;
-      bool ok = false;
-      if (!tc.force_exact) ok = fast_block<MODE>(x, bmax, tc, ld, o);
-      if (__builtin_expect(!ok, 0)) {
-        double xd[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          xd[i] = (double)ld(i);
-          nonfinite |= !(fabs(xd[i]) <= 3.4028234663852886e38);
+  uint32_t t = all_exact ? total : gw;  // all_exact: the whole tensor goes to the exact pass below
+  int s = 0;
+  uint32_t parity = 0;
+  uint32_t ndefer = 0;  // warp-uniform
+  while (true) {
+    // ---- hot loop: stream segments until done or the defer list is half full ----
+    for (; t < total && ndefer <= kDefer - 128; t += G) {
+      mbar_wait(&wb[s], parity);
+      const uint32_t kb0 = seg * (kSegElems / 16);
+      const uint32_t nbs = min((uint32_t)(kSegElems / 16), nb - kb0);  // blocks in this segment
+      const uint64_t rb = (uint64_t)row * nb;
+#pragma unroll kKbUnroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t bi = lane + 32 * j;
+        const bool valid = bi < nbs;
+        const uint32_t blk_addr = wsm + s * kTileBytes + bi * (16 * kEsz);
+        BlockOut o;
+        bool ok = true;
+        if (valid) {
+          float2 x[8];
+          float bmax;
+          load_block<DT>(blk_addr, x, bmax);
+          ok = fast_block<MODE>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
         }
-        exact_block(xd, alpha_d, MODE, p.rule, &o);
+        const uint32_t defer_mask = __ballot_sync(0xFFFFFFFFu, !ok);
+        if (__builtin_expect(defer_mask != 0, 0)) {
+          if (!ok) dl[ndefer + __popc(defer_mask & ((1u << lane) - 1))] = (uint32_t)(rb + kb0 + bi);
+          ndefer += __popc(defer_mask);
+        }
+        if (valid && ok) {
+          const uint32_t kbg = kb0 + bi;
+          *reinterpret_cast<uint64_t*>(p.codes + (rb + kbg) * 8) = o.codes;
+          p.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
+          if (p.scales_rm) p.scales_rm[rb + kbg] = (uint8_t)o.sc;
+          if (p.pick4) p.pick4[rb + kbg] = (uint8_t)o.pick4;
+        }
       }
-      codes[kb] = o.codes;
-      scw |= o.sc << (8 * kb);
-      pkw |= o.pick4 << (8 * kb);
+      __syncwarp();
+      if (lane == 0) {
+        if (tnext < total) issue(s, irow, iseg);
+        tnext += G;
+        advance(irow, iseg);
+      }
+      if (++s == kStages) {
+        s = 0;
+        parity ^= 1u;
+      }
+      advance(row, seg);
+    }
+    // ---- deferred blocks: exact float64 path (outside the hot loop) ----
+    __syncwarp();
+    if (ndefer) {
+      const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
+      const double a = resolve_alpha(p);
+      for (uint32_t i = lane; i < ndefer; i += 32) exact_block_global<DT>(ea, a, dl[i], kb4, p.d_flags);
     }
     __syncwarp();
-    if (lane == 0 && t + kStages * G < total) issue(s, t + kStages * G);
-
-    const bool live = grow < p.rows;
-    const int64_t rt = grow >> 7;
-    *reinterpret_cast<uint32_t*>(p.scales_tc + (rt * n_ct + ct) * 512 + (lane & 31) * 16 +
-                                 ((grow & 127) >> 5) * 4) = live ? scw : 0u;
-    if (live) {
-      uint4* dst = reinterpret_cast<uint4*>(p.codes + grow * (p.cols >> 1) + ct * 32);
-      dst[0] = make_uint4((uint32_t)codes[0], (uint32_t)(codes[0] >> 32), (uint32_t)codes[1],
-                          (uint32_t)(codes[1] >> 32));
-      dst[1] = make_uint4((uint32_t)codes[2], (uint32_t)(codes[2] >> 32), (uint32_t)codes[3],
-                          (uint32_t)(codes[3] >> 32));
-      if (p.scales_rm) *reinterpret_cast<uint32_t*>(p.scales_rm + grow * nb + ct * 4) = scw;
-      if (p.pick4) *reinterpret_cast<uint32_t*>(p.pick4 + grow * nb + ct * 4) = pkw;
-    }
+    ndefer = 0;
+    if (t >= total) break;
   }
-  // 32-row groups that only exist as padding of the last 128-row scale tile
-  const uint32_t n_rg_pad = (uint32_t)(((p.rows + 127) >> 7) << 2);
-  for (uint32_t t = n_rg * n_ct + gw; t < n_rg_pad * n_ct; t += G) {
-    const uint32_t rg = t / n_ct, ct = t - rg * n_ct;
-    const int64_t grow = (int64_t)rg * 32 + lane;
-    *reinterpret_cast<uint32_t*>(p.scales_tc + ((grow >> 7) * n_ct + ct) * 512 + lane * 16 +
-                                 ((grow & 127) >> 5) * 4) = 0u;
+  if (all_exact) {
+    // alpha outside the fast path's range / rule != mse: every block exactly
+    const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
+    const uint32_t nblk = (uint32_t)p.rows * nb;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
+      exact_block_global<DT>(ea, alpha_d, b, kb4, p.d_flags);
+  }
+  // tcgen05 layout padding: kb in [nb, 4*kb4) of every row, rows up to a multiple of 128
+  const uint32_t rows = (uint32_t)p.rows, rows_pad = (rows + 127) & ~127u;
+  const uint32_t kpad = 4 * kb4 - nb;
+  const uint32_t n_a = rows * kpad, n_b = (rows_pad - rows) * 4 * kb4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_a + n_b; i += gridDim.x * blockDim.x) {
+    uint32_t r, kb;
+    if (i < n_a) {
+      r = i / kpad;
+      kb = nb + (i - r * kpad);
+    } else {
+      r = rows + (i - n_a) / (4 * kb4);
+      kb = (i - n_a) - (r - rows) * 4 * kb4;
+    }
+    p.scales_tc[sf_tc_offset(r, kb, kb4)] = 0;
   }
   if (nonfinite && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
 }
@@ -561,36 +677,24 @@ int launch_status() {
 }
 
 template <int DT, int MODE>
-int launch_quant_tma(const QParams& p, cudaStream_t s) {
-  EncodeTiledFn enc = get_encode_fn();
-  if (!enc) return F46_ERR_UNSUPPORTED;
-  CUtensorMap map;
-  const int esz = DT == DT_BF16 ? 2 : 4;
-  cuuint64_t dims[2] = {(cuuint64_t)p.cols, (cuuint64_t)p.rows};
-  cuuint64_t strides[1] = {(cuuint64_t)(p.cols * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(&map, DT == DT_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                   2, const_cast<void*>(p.x), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return F46_ERR_UNSUPPORTED;
-  constexpr int kTileBytes = (DT == DT_BF16) ? 4096 : 8192;
-  const int smem = kWarps * kStages * kTileBytes + 1024;
+int launch_quant_seg(const QParams& p, cudaStream_t s) {
+  constexpr int kTileBytes = kSegElems * ((DT == DT_BF16) ? 2 : 4);
+  const int smem = kWarps * kStages * kTileBytes;
   static bool configured = false;
   static int ctas_per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(quant_tma_kernel<DT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(quant_seg_kernel<DT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_tma_kernel<DT, MODE>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_seg_kernel<DT, MODE>,
                                                   kWarps * 32, smem);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
     configured = true;
   }
-  const int64_t wtiles = (p.cols >> 6) * ((p.rows + 127) >> 7) * 4;
-  int64_t grid = (wtiles + kWarps - 1) / kWarps;
+  const int64_t tiles = p.rows * ((p.cols + kSegElems - 1) / kSegElems);
+  int64_t grid = (tiles + kWarps - 1) / kWarps;
   if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
-  quant_tma_kernel<DT, MODE><<<(unsigned)grid, kWarps * 32, smem, s>>>(map, p);
+  if (grid < 1) grid = 1;
+  quant_seg_kernel<DT, MODE><<<(unsigned)grid, kWarps * 32, smem, s>>>(p);
   return launch_status();
 }
 
@@ -609,11 +713,11 @@ template <int DT>
 int dispatch_mode(const QParams& p, cudaStream_t s, bool tma) {
   switch (p.mode) {
     case F46_FIXED6:
-      return tma ? launch_quant_tma<DT, FIXED6>(p, s) : launch_quant_generic<DT, FIXED6>(p, s);
+      return tma ? launch_quant_seg<DT, FIXED6>(p, s) : launch_quant_generic<DT, FIXED6>(p, s);
     case F46_FIXED4:
-      return tma ? launch_quant_tma<DT, FIXED4>(p, s) : launch_quant_generic<DT, FIXED4>(p, s);
+      return tma ? launch_quant_seg<DT, FIXED4>(p, s) : launch_quant_generic<DT, FIXED4>(p, s);
     default:
-      return tma ? launch_quant_tma<DT, ADAPTIVE>(p, s) : launch_quant_generic<DT, ADAPTIVE>(p, s);
+      return tma ? launch_quant_seg<DT, ADAPTIVE>(p, s) : launch_quant_generic<DT, ADAPTIVE>(p, s);
   }
 }
 
@@ -671,10 +775,10 @@ int f46_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int mode,
   QParams p{x, rows, cols, mode, rule, dtype, mcap, d_amax, alpha_override, codes, scales_tc,
             scales_rm, pick4, d_alpha_out, d_flags};
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tma = (dtype != F46_DT_F64) && (cols % 64 == 0) && (((uintptr_t)x & 15) == 0) &&
-                   (((uintptr_t)codes & 15) == 0) && (((uintptr_t)scales_tc & 3) == 0) &&
-                   (((uintptr_t)scales_rm & 3) == 0) && (((uintptr_t)pick4 & 3) == 0) &&
-                   rows < (1ll << 31) && cols < (1ll << 31);
+  // segment kernel: 16-element blocks never straddle rows, 16-byte aligned rows
+  const bool tma = (dtype != F46_DT_F64) && (cols % 16 == 0) && (((uintptr_t)x & 15) == 0) &&
+                   (((uintptr_t)codes & 7) == 0) &&
+                   rows < (1ll << 31) && cols < (1ll << 31) && rows * ((cols + 15) / 16) < (1ll << 32);
   switch (dtype) {
     case F46_DT_BF16: {
       int rc = dispatch_mode<DT_BF16>(p, s, tma);
