@@ -384,74 +384,99 @@ __device__ __forceinline__ uint32_t fix_word(uint32_t w, uint32_t dmask, int bas
   return w;
 }
 
-// r = v - q in one FHADD (f16 half + f32, single rounding), r^2 accumulated.
-__device__ __forceinline__ float fhadd(__half v, float negq) {
+// Round a quotient pair to E2M1 (cvt.rn.satfinite) and decode it straight back
+// to f16x2 without packing the codes (the candidates' codes are only needed
+// for their error; the stored candidate's codes are recomputed and packed
+// once).  The .b8 never leaves the asm block, so no byte extraction is emitted.
+__device__ __forceinline__ uint32_t e2m1x2_roundtrip(float hi, float lo) {
+  uint32_t d;
+  asm("{\n\t.reg .b8 c;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 c, %1, %2;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %0, c;\n\t}"
+      : "=r"(d)
+      : "f"(hi), "f"(lo));
+  return d;
+}
+
+// r = v - q with v one half of an f16x2 word: one mixed-precision FHADD
+// (f16 + f32 -> f32, single rounding) on the FMA pipe.
+template <int H>
+__device__ __forceinline__ float fhadd_h(uint32_t v, float negq) {
   float r;
-  asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(r) : "h"(__half_as_ushort(v)), "f"(negq));
+  if (H == 0)
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, l, %2;\n\t}"
+        : "=f"(r)
+        : "r"(v), "f"(negq));
+  else
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, h, %2;\n\t}"
+        : "=f"(r)
+        : "r"(v), "f"(negq));
   return r;
 }
 
-// One candidate on the fast path: codes of the lower-bound quotients and the
-// quotient-space squared error sum  sum_i (v_i - q_i)^2  (q_i ~ x_i/(alpha*Delta)).
-struct Cand {
-  uint32_t w0, w1;  // codes (elements 0-7, 8-15)
-  float rq;         // the lower-bound reciprocal used
-  float sq;         // quotient-space error sum
-};
+// Exact bf16 -> f32 of the high half of w on the FMA pipe (FHADD.BF16 w.H1 + -0,
+// which keeps the sign of -0.0); the low half is a shift (IMAD.SHL).
+__device__ __forceinline__ float2 bf16x2_unpack(uint32_t w) {
+  float hi;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, h, %2;\n\t}"
+      : "=f"(hi)
+      : "r"(w), "f"(-0.0f));
+  return make_float2(__uint_as_float(w << 16), hi);
+}
 
-__device__ __forceinline__ void cand_eval(const float2 (&x)[8], float D, Cand& c) {
-  c.rq = rcp_approx(D) * F46_QLO;
-  const float2 r2 = make_float2(c.rq, c.rq);
+// Quotient-space squared error of one candidate,  sum_i (v_i - q_i)^2  with
+// q_i = x_i * rq (the lower-bound reciprocal) and v_i = E2M1(q_i).  Two
+// independent f32x2 accumulators; any order of the 16 f32 additions stays
+// inside the 2^-20 relative bound the decision tolerance allows for.
+__device__ __forceinline__ float cand_err(const float2 (&x)[8], float rq) {
+  const float2 r2 = make_float2(rq, rq);
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const float2 q = __fmul2_rn(x[p], r2);
+    const uint32_t v = e2m1x2_roundtrip(q.y, q.x);
+    const float2 r = make_float2(fhadd_h<0>(v, -q.x), fhadd_h<1>(v, -q.y));
+    if (p & 1)
+      acc1 = __ffma2_rn(r, r, acc1);
+    else
+      acc0 = __ffma2_rn(r, r, acc0);
+  }
+  return (acc0.x + acc0.y) + (acc1.x + acc1.y);
+}
+
+// Packed codes of x * r (16 nibbles, element i at bits [4i, 4i+4)).
+__device__ __forceinline__ uint64_t codes_of(const float2 (&x)[8], float r) {
+  const float2 r2 = make_float2(r, r);
   float2 q[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
-  c.w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
-  c.w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]);
-  __half2 v[8];
-  v[0] = e2m1x2_to_h2<0>(c.w0);
-  v[1] = e2m1x2_to_h2<1>(c.w0);
-  v[2] = e2m1x2_to_h2<2>(c.w0);
-  v[3] = e2m1x2_to_h2<3>(c.w0);
-  v[4] = e2m1x2_to_h2<0>(c.w1);
-  v[5] = e2m1x2_to_h2<1>(c.w1);
-  v[6] = e2m1x2_to_h2<2>(c.w1);
-  v[7] = e2m1x2_to_h2<3>(c.w1);
-  float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    const float2 r = make_float2(fhadd(__low2half(v[p]), -q[p].x), fhadd(__high2half(v[p]), -q[p].y));
-    acc = __ffma2_rn(r, r, acc);
-  }
-  c.sq = acc.x + acc.y;
+  const uint32_t w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  const uint32_t w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]);
+  return ((uint64_t)w1 << 32) | w0;
 }
 
-// Exact codes for the stored candidate.  w0/w1 are the codes of the strict
-// lower-bound quotient q; the codes of the strict upper bound q*QHI/QLO agree
-// with them except at nibbles whose bracket straddles an FP4 tie, where the
-// true code is one of the two.  With a known tensor-wide tie direction the
-// choice is a word select; otherwise each flagged nibble gets the exact test.
+// Exact codes of the stored candidate from its lower-bound reciprocal rq.
+// q = x*rq is a strict lower bound of the true quotient x/(alpha*Delta) and
+// q*QHI/QLO a strict upper bound; their codes agree except at nibbles whose
+// bracket straddles an FP4 tie, where the true code is one of the two.  With a
+// known tensor-wide tie direction one of the two bounds is already exact;
+// otherwise both are formed and each flagged nibble is settled exactly.
 template <class Load>
-__device__ __forceinline__ uint64_t exact_codes(const float2 (&x)[8], uint32_t w0, uint32_t w1,
-                                                float rq, float alpha, float delta, int tdir,
-                                                const Load& load) {
-  if (tdir < 0) return ((uint64_t)w1 << 32) | w0;
+__device__ __forceinline__ uint64_t exact_codes(const float2 (&x)[8], float rq, float alpha,
+                                                float delta, int tdir, const Load& load) {
   const float rh = rq * F46_QHI_OVER_QLO;
-  const float2 rh2 = make_float2(rh, rh);
-  float2 qh[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) qh[p] = __fmul2_rn(x[p], rh2);
-  const uint32_t h0 = cvt_e2m1x8(qh[0], qh[1], qh[2], qh[3]);
-  const uint32_t h1 = cvt_e2m1x8(qh[4], qh[5], qh[6], qh[7]);
-  if (tdir == 1) return ((uint64_t)h1 << 32) | h0;
+  if (tdir < 0) return codes_of(x, rq);
+  if (tdir == 1) return codes_of(x, rh);
+  const uint64_t lo = codes_of(x, rq), hi = codes_of(x, rh);
+  uint32_t w0 = (uint32_t)lo, w1 = (uint32_t)(lo >> 32);
+  const uint32_t h0 = (uint32_t)hi, h1 = (uint32_t)(hi >> 32);
   const uint32_t d0 = w0 ^ h0, d1 = w1 ^ h1;
   if (tdir == 0) {
-    // exact ties: take the upper code where the lower one has an odd magnitude
-    auto even = [](uint32_t lo, uint32_t hi, uint32_t d) {
-      const uint32_t flag = (d | (d >> 1) | (d >> 2) | (d >> 3)) & 0x11111111u;
-      const uint32_t up = (flag & lo) * 0xFu;
-      return (lo & ~up) | (hi & up);
-    };
-    return ((uint64_t)even(w1, h1, d1) << 32) | even(w0, h0, d0);
+    // Exact ties: a flagged nibble holds the lower code m (q's side) and the
+    // upper code m+1 (magnitude m <= 6, so no carry leaves the nibble).  If m
+    // is even, only bit 0 differs; if m is odd the increment carries into
+    // bit 1.  Adding bit 1 of the difference therefore selects the even code.
+    return ((uint64_t)(w1 + ((d1 & 0x22222222u) >> 1)) << 32) | (w0 + ((d0 & 0x22222222u) >> 1));
   }
   if (__builtin_expect((d0 | d1) != 0, 0)) {
     w0 = fix_word(w0, d0, 0, alpha, delta, load);
@@ -466,7 +491,10 @@ __device__ __forceinline__ uint64_t exact_codes(const float2 (&x)[8], uint32_t w
 template <int MODE, class Load>
 __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, const TensorConsts& tc,
                                            const Load& load, BlockOut& out) {
-  if (bmax == 0.f) {
+  // One unsigned compare keeps bmax in [2^-40, 2^40) (NaN and +-inf fail it).
+  const uint32_t bb = __float_as_uint(bmax);
+  if (__builtin_expect(bb - 0x2B800000u >= 0x28000000u, 0)) {
+    if (bb != 0u) return false;
     // All-zero block: scale code 1 (blockquant.py:241), codes carry the sign
     // bit of -0.0 (codecs.py:109,116), both errors 0 -> tie keeps 6.
     uint64_t c = 0;
@@ -480,7 +508,6 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
     out.pick4 = (MODE == FIXED4);
     return true;
   }
-  if (!(bmax >= 0x1p-40f && bmax <= 0x1p40f)) return false;
   const float alpha = tc.alpha;
   if (MODE == FIXED6 || MODE == FIXED4) {
     const float m = MODE == FIXED6 ? 6.f : 4.f;
@@ -489,42 +516,108 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
     if (sc == 0) return false;
     const float delta = e4m3_to_f32(sc);
     const float rq = rcp_approx(alpha * delta) * F46_QLO;
-    const float2 r2 = make_float2(rq, rq);
-    float2 q[8];
-#pragma unroll
-    for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
-    out.codes = exact_codes(x, cvt_e2m1x8(q[0], q[1], q[2], q[3]), cvt_e2m1x8(q[4], q[5], q[6], q[7]),
-                            rq, alpha, delta, tc.tdir, load);
+    out.codes = exact_codes(x, rq, alpha, delta, tc.tdir, load);
     out.sc = sc;
     out.pick4 = (MODE == FIXED4);
     return true;
   } else {
-    const uint32_t sc6 = block_scale_code(bmax, alpha, 6.f, tc.r6_lo, tc.r6_hi);
-    const uint32_t sc4 = block_scale_code(bmax, alpha, 4.f, tc.r4_lo, tc.r4_hi);
-    if (sc6 == 0 || sc4 == 0) return false;
-    const float d6 = e4m3_to_f32(sc6), d4 = e4m3_to_f32(sc4);
-    const float D6 = alpha * d6, D4 = alpha * d4;
-    Cand c6, c4;
-    cand_eval(x, D6, c6);
-    cand_eval(x, D4, c4);
+    // Both candidates' scale codes from one pair of bracketing quotients
+    // (low byte: M=6, high byte: M=4).  A disagreement means bmax/(alpha*m)
+    // lies within 2^-17 of an E4M3 tie; such blocks (and underflowed scales,
+    // code 0 -- the M=4 code is never below the M=6 one) go to the exact path.
+    const float2 b2 = make_float2(bmax, bmax);
+    const float2 th = __fmul2_rn(b2, make_float2(tc.r6_hi, tc.r4_hi));
+    const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
+    const uint32_t ph = cvt_e4m3x2(th.y, th.x), pl = cvt_e4m3x2(tl.y, tl.x);
+    if (__builtin_expect(ph != pl || (pl & 0xFFu) == 0u, 0)) return false;
+    uint32_t dd;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(dd) : "h"((uint16_t)pl));
+    const float2 dlt = make_float2(fhadd_h<0>(dd, -0.f), fhadd_h<1>(dd, -0.f));  // exact
+    const float2 D = __fmul2_rn(make_float2(alpha, alpha), dlt);
+    const float2 rq = __fmul2_rn(make_float2(rcp_approx(D.x), rcp_approx(D.y)),
+                                 make_float2(F46_QLO, F46_QLO));
+    const float2 sq = make_float2(cand_err(x, rq.x), cand_err(x, rq.y));
     // x-space sums S_m = D_m^2 * sq_m.  Certified bound on |S_m(f32) - S_m(ref)|
     // (DESIGN.md section "decision bound"): quotient error 2^-19.9 ->
     // 2^-18.9 * sqrt(S_m * sum x^2) <= 2^-16.9 * bmax * sqrt(S_m); codes taken
     // from the lower-bound quotient can differ from the exact ones only at
     // near-ties, moving S_m by <= 2^-15.1 * S_m; f32 rounding <= 2^-20 * S_m;
-    // second-order quotient terms <= 2^-33.8 * bmax^2.
-    const float s6 = c6.sq * (D6 * D6), s4 = c4.sq * (D4 * D4);
-    const float tol = 0x1p-16f * bmax * (sqrt_approx(s6) + sqrt_approx(s4)) +
-                      0x1p-14f * (s6 + s4) + 0x1p-32f * (bmax * bmax) + 0x1p-140f;
-    if (__builtin_expect(fabsf(s6 - s4) <= tol, 0)) return false;  // exact path decides
-    const bool k = s4 < s6;
-    const float delta = k ? d4 : d6;
-    out.codes = exact_codes(x, k ? c4.w0 : c6.w0, k ? c4.w1 : c6.w1, k ? c4.rq : c6.rq, alpha,
-                            delta, tc.tdir, load);
-    out.sc = k ? sc4 : sc6;
+    // second-order quotient terms <= 2^-33.8 * bmax^2.  The first term is
+    // covered through sqrt(s6) + sqrt(s4) <= sqrt(2 * (s6 + s4)).
+    const float2 s = __fmul2_rn(sq, __fmul2_rn(D, D));
+    const float ssum = s.x + s.y;
+    const float tol = fmaf(0x1p-15f * bmax, sqrt_approx(ssum),
+                           fmaf(0x1p-14f, ssum, fmaf(0x1p-32f * bmax, bmax, 0x1p-140f)));
+    if (__builtin_expect(fabsf(s.x - s.y) <= tol, 0)) return false;  // exact path decides
+    const bool k = s.y < s.x;
+    out.codes = exact_codes(x, k ? rq.y : rq.x, alpha, k ? dlt.y : dlt.x, tc.tdir, load);
+    out.sc = k ? (pl >> 8) : (pl & 0xFFu);
     out.pick4 = k;
     return true;
   }
+}
+
+// Straight-line variant of fast_block for the streaming kernel, with the
+// tensor-wide tie direction as a template parameter (TDIR: -1, 0, +1, or 2 =
+// unknown).  No early exits: every condition that sends a block to the exact
+// path (all-zero or out-of-range bmax, near-tie or underflowed scale code,
+// ambiguous 4/6 decision) folds into the returned flag, so consecutive blocks
+// of one lane can be scheduled together.  Same arithmetic and bounds as
+// fast_block.
+template <int TDIR, class Load>
+__device__ __forceinline__ uint64_t codes_dir(const float2 (&x)[8], float rq, float alpha,
+                                              float delta, const Load& load) {
+  if constexpr (TDIR < 0) {
+    return codes_of(x, rq);
+  } else if constexpr (TDIR == 1) {
+    return codes_of(x, rq * F46_QHI_OVER_QLO);
+  } else {
+    return exact_codes(x, rq, alpha, delta, TDIR, load);
+  }
+}
+
+template <int MODE, int TDIR, class Load>
+__device__ __forceinline__ bool block_sl(const float2 (&x)[8], float bmax, const TensorConsts& tc,
+                                         const Load& load, BlockOut& out) {
+  const uint32_t bb = __float_as_uint(bmax);
+  bool ok = (bb - 0x2B800000u) < 0x28000000u;  // bmax in [2^-40, 2^40)
+  const float alpha = tc.alpha;
+  if constexpr (MODE == FIXED6 || MODE == FIXED4) {
+    const float2 t = __fmul2_rn(make_float2(bmax, bmax), MODE == FIXED6
+                                                             ? make_float2(tc.r6_hi, tc.r6_lo)
+                                                             : make_float2(tc.r4_hi, tc.r4_lo));
+    const uint32_t pr = cvt_e4m3x2(t.x, t.y);  // low byte: lower bracket
+    const uint32_t sc = pr & 0xFFu;
+    ok &= ((pr >> 8) == sc) & (sc != 0u);
+    const float delta = e4m3_to_f32(sc);
+    const float rq = rcp_approx(alpha * delta) * F46_QLO;
+    out.codes = codes_dir<TDIR>(x, rq, alpha, delta, load);
+    out.sc = sc;
+    out.pick4 = (MODE == FIXED4);
+  } else {
+    const float2 b2 = make_float2(bmax, bmax);
+    const float2 th = __fmul2_rn(b2, make_float2(tc.r6_hi, tc.r4_hi));
+    const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
+    const uint32_t ph = cvt_e4m3x2(th.y, th.x), pl = cvt_e4m3x2(tl.y, tl.x);
+    ok &= (ph == pl) & ((pl & 0xFFu) != 0u);
+    uint32_t dd;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(dd) : "h"((uint16_t)pl));
+    const float2 dlt = make_float2(fhadd_h<0>(dd, -0.f), fhadd_h<1>(dd, -0.f));
+    const float2 D = __fmul2_rn(make_float2(alpha, alpha), dlt);
+    const float2 rq = __fmul2_rn(make_float2(rcp_approx(D.x), rcp_approx(D.y)),
+                                 make_float2(F46_QLO, F46_QLO));
+    const float2 sq = make_float2(cand_err(x, rq.x), cand_err(x, rq.y));
+    const float2 s = __fmul2_rn(sq, __fmul2_rn(D, D));
+    const float ssum = s.x + s.y;
+    const float tol = fmaf(0x1p-15f * bmax, sqrt_approx(ssum),
+                           fmaf(0x1p-14f, ssum, fmaf(0x1p-32f * bmax, bmax, 0x1p-140f)));
+    ok &= fabsf(s.x - s.y) > tol;  // NaN (from a rejected block) compares false
+    const bool k = s.y < s.x;
+    out.codes = codes_dir<TDIR>(x, k ? rq.y : rq.x, alpha, k ? dlt.y : dlt.x, load);
+    out.sc = k ? (pl >> 8) : (pl & 0xFFu);
+    out.pick4 = k;
+  }
+  return ok;
 }
 
 // ----------------------------------------------------------------------------

@@ -28,7 +28,10 @@ using namespace f46;
 
 namespace {
 
-constexpr int kStages = 3;
+#ifndef F46_STAGES
+#define F46_STAGES 3
+#endif
+constexpr int kStages = F46_STAGES;
 
 int g_num_sms = 0;
 
@@ -155,8 +158,7 @@ __device__ __forceinline__ void load_block(uint32_t blk, float2 (&x)[8], float& 
     const uint4 b = lds128(blk + 16);
     const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
-      x[p] = make_float2(__uint_as_float(w[p] << 16), __uint_as_float(w[p] & 0xFFFF0000u));
+    for (int p = 0; p < 8; ++p) x[p] = bf16x2_unpack(w[p]);
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -188,7 +190,10 @@ __device__ __forceinline__ void load_block(uint32_t blk, float2 (&x)[8], float& 
 // shared list and recomputed exactly outside the hot loop.
 // ---------------------------------------------------------------------------
 constexpr int kWarps = 4;
-constexpr int kSegElems = 2048;
+#ifndef F46_SEG
+#define F46_SEG 2048
+#endif
+constexpr int kSegElems = F46_SEG;
 #ifndef F46_KB_UNROLL
 #define F46_KB_UNROLL 1
 #endif
@@ -236,21 +241,150 @@ __device__ __forceinline__ void exact_block_global(ExactArgs a, double alpha, ui
     else
       xd[i] = (double)reinterpret_cast<const float*>(a.x)[row * a.cols + c];
   }
-  bool nf = false;
+  bool nf = false, zero = true;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) nf |= !(fabs(xd[i]) <= 3.4028234663852886e38);
+  for (int i = 0; i < 16; ++i) {
+    nf |= !(fabs(xd[i]) <= 3.4028234663852886e38);
+    zero &= (xd[i] == 0.0);
+  }
   if (nf && nonfinite) atomicOr(nonfinite, F46_FLAG_NONFINITE);
   BlockOut o;
-  exact_block_inl(xd, alpha, a.mode, a.rule, &o);
+  if (zero) {
+    // all-zero block (blockquant.py:241): scale code 1, codes keep the sign of -0.0
+    // (codecs.py:109,116); both candidate errors are 0, so the tie keeps 6.
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c |= (uint64_t)(signbit(xd[i]) ? 8u : 0u) << (4 * i);
+    o.codes = c;
+    o.sc = 1;
+    o.pick4 = (a.mode == FIXED4);
+  } else {
+    exact_block_inl(xd, alpha, a.mode, a.rule, &o);
+  }
   *reinterpret_cast<uint64_t*>(a.codes + (row * nb + kbg) * 8) = o.codes;
   a.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
   if (a.scales_rm) a.scales_rm[row * nb + kbg] = (uint8_t)o.sc;
   if (a.pick4) a.pick4[row * nb + kbg] = (uint8_t)o.pick4;
 }
 
-constexpr int kDefer = 256;  // deferred-block slots per warp (a segment defers <= 128)
+constexpr int kBPL = kSegElems / 512;   // blocks per lane per segment
+constexpr int kDefer = 2 * kSegElems / 16;  // deferred-block slots per warp (a segment defers <= half)
 
-template <int DT, int MODE>
+// The streaming loop of one warp, specialised on the tensor-wide tie direction.
+template <int DT, int MODE, bool EXTRA, int TDIR>
+__device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts& tc, uint32_t wsm,
+                                           uint64_t* wb, uint32_t* dl, uint32_t t_begin,
+                                           uint32_t t_end) {
+  constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
+  constexpr int kTileBytes = kSegElems * kEsz;
+  constexpr uint32_t kSegBlocks = kSegElems / 16;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cols = (uint32_t)p.cols;
+  const uint32_t nb = cols >> 4;
+  const uint32_t kb4 = (nb + 3) >> 2;
+  const uint32_t n_seg = (cols + kSegElems - 1) / kSegElems;
+
+  // Each warp streams one contiguous range of tiles (tile = one segment of one
+  // row): successive tiles are adjacent in memory, so cursors only step.
+  const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
+  uint32_t irow = t_begin / n_seg, iseg = t_begin - irow * n_seg;  // next tile to issue
+  uint32_t tnext = t_begin;
+  auto issue = [&](int s) {
+    if (tnext < t_end) {
+      const uint32_t c0 = iseg * kSegElems;
+      const uint32_t n = min((uint32_t)kSegElems, cols - c0);
+      mbar_expect_tx(&wb[s], n * kEsz);
+      bulk_load(wsm + s * kTileBytes, xb + ((uint64_t)irow * cols + c0) * kEsz, n * kEsz, &wb[s]);
+    }
+    ++tnext;
+    if (++iseg == n_seg) {
+      iseg = 0;
+      ++irow;
+    }
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) issue(s);
+  }
+  uint32_t row = t_begin / n_seg, seg = t_begin - row * n_seg;  // tile being consumed
+
+  uint32_t t = t_begin;
+  int s = 0;
+  uint32_t parity = 0;
+  uint32_t ndefer = 0;  // warp-uniform
+  while (true) {
+    // ---- hot loop: stream segments until done or the defer list is half full ----
+    for (; t < t_end && ndefer <= kDefer - kSegBlocks; ++t) {
+      mbar_wait(&wb[s], parity);
+      const uint32_t kb0 = seg * kSegBlocks;                // a multiple of 4
+      const uint32_t nbs = min(kSegBlocks, nb - kb0);       // blocks in this segment
+      const uint64_t rbk = (uint64_t)row * nb + kb0;        // first block of the segment
+      // Per-lane output cursors: lane l owns blocks kb0 + l + 32j, whose codes
+      // sit 256 B apart and whose tcgen05-layout scales sit 8 tiles (4 KB) apart.
+      uint8_t* cptr = p.codes + (rbk + lane) * 8;
+      uint8_t* sptr = p.scales_tc +
+                      ((uint64_t)(row >> 7) * kb4 + (kb0 >> 2) + (lane >> 2)) * 512 +
+                      (row & 31) * 16 + ((row & 127) >> 5) * 4 + (lane & 3);
+      const uint32_t blk0 = wsm + s * kTileBytes + lane * (16 * kEsz);
+      uint32_t fails = 0;
+      auto one = [&](int j) {
+        const uint32_t blk_addr = blk0 + j * (32 * 16 * kEsz);
+        float2 x[8];
+        float bmax;
+        load_block<DT>(blk_addr, x, bmax);
+        BlockOut o;
+        if (block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o)) {
+          *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
+          sptr[j * 4096] = (uint8_t)o.sc;
+          if constexpr (EXTRA) {
+            if (p.scales_rm) p.scales_rm[rbk + lane + 32 * j] = (uint8_t)o.sc;
+            if (p.pick4) p.pick4[rbk + lane + 32 * j] = (uint8_t)o.pick4;
+          }
+        } else {
+          fails |= 1u << j;
+        }
+      };
+      if (nbs == kSegBlocks) {
+#pragma unroll kKbUnroll
+        for (int j = 0; j < kBPL; ++j) one(j);
+      } else {
+        for (int j = 0; j < kBPL; ++j)
+          if (lane + 32 * j < nbs) one(j);
+      }
+      if (__builtin_expect(__any_sync(0xFFFFFFFFu, fails != 0), 0)) {
+#pragma unroll
+        for (int j = 0; j < kBPL; ++j) {
+          const bool f = (fails >> j) & 1u;
+          const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+          if (f) dl[ndefer + __popc(m & ((1u << lane) - 1))] = (uint32_t)(rbk + lane + 32 * j);
+          ndefer += __popc(m);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) issue(s);
+      if (++s == kStages) {
+        s = 0;
+        parity ^= 1u;
+      }
+      if (++seg == n_seg) {
+        seg = 0;
+        ++row;
+      }
+    }
+    // ---- deferred blocks: exact float64 path (outside the hot loop) ----
+    __syncwarp();
+    if (ndefer) {
+      const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
+      const double a = resolve_alpha(p);
+      for (uint32_t i = lane; i < ndefer; i += 32) exact_block_global<DT>(ea, a, dl[i], kb4, p.d_flags);
+    }
+    __syncwarp();
+    ndefer = 0;
+    if (t >= t_end) break;
+  }
+}
+
+template <int DT, int MODE, bool EXTRA>
 __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParams p) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
   constexpr int kTileBytes = kSegElems * kEsz;
@@ -272,7 +406,6 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   const TensorConsts tc = make_consts(
       alpha_d, p.rule, DT,
       tie_direction(alpha_d, overridden ? 0.0 : *p.d_amax, p.mcap, DT, overridden));
-  const bool all_exact = tc.force_exact;
 
   const uint32_t wsm = smem_u32(smem) + warp * (kStages * kTileBytes);
   uint64_t* wb = bars[warp];
@@ -284,102 +417,31 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   }
   __syncwarp();
 
-  const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
-  auto issue = [&](int s, uint32_t row, uint32_t seg) {
-    const uint32_t c0 = seg * kSegElems;
-    const uint32_t n = min((uint32_t)kSegElems, cols - c0);
-    mbar_expect_tx(&wb[s], n * kEsz);
-    bulk_load(wsm + s * kTileBytes, xb + ((uint64_t)row * cols + c0) * kEsz, n * kEsz, &wb[s]);
-  };
-  // (row, seg) of tile t, advanced by G = g_row * n_seg + g_seg without division
-  const uint32_t g_row = G / n_seg, g_seg = G - g_row * n_seg;
-  auto advance = [&](uint32_t& row, uint32_t& seg) {
-    row += g_row;
-    seg += g_seg;
-    if (seg >= n_seg) {
-      seg -= n_seg;
-      ++row;
-    }
-  };
-  uint32_t row = gw / n_seg, seg = gw - (gw / n_seg) * n_seg;  // tile being consumed
-  uint32_t irow = row, iseg = seg;                             // next tile to issue
-  uint32_t tnext = gw;
-  if (lane == 0 && !all_exact) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s) {
-      if (tnext < total) issue(s, irow, iseg);
-      tnext += G;
-      advance(irow, iseg);
-    }
-  }
-
-  bool nonfinite = false;
-  uint32_t t = all_exact ? total : gw;  // all_exact: the whole tensor goes to the exact pass below
-  int s = 0;
-  uint32_t parity = 0;
-  uint32_t ndefer = 0;  // warp-uniform
-  while (true) {
-    // ---- hot loop: stream segments until done or the defer list is half full ----
-    for (; t < total && ndefer <= kDefer - 128; t += G) {
-      mbar_wait(&wb[s], parity);
-      const uint32_t kb0 = seg * (kSegElems / 16);
-      const uint32_t nbs = min((uint32_t)(kSegElems / 16), nb - kb0);  // blocks in this segment
-      const uint64_t rb = (uint64_t)row * nb;
-#pragma unroll kKbUnroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t bi = lane + 32 * j;
-        const bool valid = bi < nbs;
-        const uint32_t blk_addr = wsm + s * kTileBytes + bi * (16 * kEsz);
-        BlockOut o;
-        bool ok = true;
-        if (valid) {
-          float2 x[8];
-          float bmax;
-          load_block<DT>(blk_addr, x, bmax);
-          ok = fast_block<MODE>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
-        }
-        const uint32_t defer_mask = __ballot_sync(0xFFFFFFFFu, !ok);
-        if (__builtin_expect(defer_mask != 0, 0)) {
-          if (!ok) dl[ndefer + __popc(defer_mask & ((1u << lane) - 1))] = (uint32_t)(rb + kb0 + bi);
-          ndefer += __popc(defer_mask);
-        }
-        if (valid && ok) {
-          const uint32_t kbg = kb0 + bi;
-          *reinterpret_cast<uint64_t*>(p.codes + (rb + kbg) * 8) = o.codes;
-          p.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
-          if (p.scales_rm) p.scales_rm[rb + kbg] = (uint8_t)o.sc;
-          if (p.pick4) p.pick4[rb + kbg] = (uint8_t)o.pick4;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        if (tnext < total) issue(s, irow, iseg);
-        tnext += G;
-        advance(irow, iseg);
-      }
-      if (++s == kStages) {
-        s = 0;
-        parity ^= 1u;
-      }
-      advance(row, seg);
-    }
-    // ---- deferred blocks: exact float64 path (outside the hot loop) ----
-    __syncwarp();
-    if (ndefer) {
-      const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
-      const double a = resolve_alpha(p);
-      for (uint32_t i = lane; i < ndefer; i += 32) exact_block_global<DT>(ea, a, dl[i], kb4, p.d_flags);
-    }
-    __syncwarp();
-    ndefer = 0;
-    if (t >= total) break;
-  }
-  if (all_exact) {
+  const uint32_t per = total / G, rem = total - per * G;
+  const uint32_t t_begin = gw * per + min(gw, rem);
+  const uint32_t t_end = t_begin + per + (gw < rem ? 1u : 0u);
+  if (tc.force_exact) {
     // alpha outside the fast path's range / rule != mse: every block exactly
     const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
     const uint32_t nblk = (uint32_t)p.rows * nb;
     for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
       exact_block_global<DT>(ea, alpha_d, b, kb4, p.d_flags);
+  } else if constexpr (DT == DT_BF16) {
+    switch (tc.tdir) {
+      case -1:
+        seg_stream<DT, MODE, EXTRA, -1>(p, tc, wsm, wb, dl, t_begin, t_end);
+        break;
+      case 0:
+        seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end);
+        break;
+      case 1:
+        seg_stream<DT, MODE, EXTRA, 1>(p, tc, wsm, wb, dl, t_begin, t_end);
+        break;
+      default:
+        seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end);
+    }
+  } else {
+    seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end);
   }
   // tcgen05 layout padding: kb in [nb, 4*kb4) of every row, rows up to a multiple of 128
   const uint32_t rows = (uint32_t)p.rows, rows_pad = (rows + 127) & ~127u;
@@ -396,7 +458,6 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
     }
     p.scales_tc[sf_tc_offset(r, kb, kb4)] = 0;
   }
-  if (nonfinite && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
 }
 
 // ---------------------------------------------------------------------------
@@ -676,16 +737,16 @@ int launch_status() {
   return F46_OK;
 }
 
-template <int DT, int MODE>
+template <int DT, int MODE, bool EXTRA>
 int launch_quant_seg(const QParams& p, cudaStream_t s) {
   constexpr int kTileBytes = kSegElems * ((DT == DT_BF16) ? 2 : 4);
   const int smem = kWarps * kStages * kTileBytes;
   static bool configured = false;
   static int ctas_per_sm = 1;
   if (!configured) {
-    cudaFuncSetAttribute(quant_seg_kernel<DT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(quant_seg_kernel<DT, MODE, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_seg_kernel<DT, MODE>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_seg_kernel<DT, MODE, EXTRA>,
                                                   kWarps * 32, smem);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
     configured = true;
@@ -694,7 +755,7 @@ int launch_quant_seg(const QParams& p, cudaStream_t s) {
   int64_t grid = (tiles + kWarps - 1) / kWarps;
   if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
   if (grid < 1) grid = 1;
-  quant_seg_kernel<DT, MODE><<<(unsigned)grid, kWarps * 32, smem, s>>>(p);
+  quant_seg_kernel<DT, MODE, EXTRA><<<(unsigned)grid, kWarps * 32, smem, s>>>(p);
   return launch_status();
 }
 
@@ -709,15 +770,23 @@ int launch_quant_generic(const QParams& p, cudaStream_t s) {
   return launch_status();
 }
 
+template <int DT, int MODE>
+int launch_quant(const QParams& p, cudaStream_t s, bool tma) {
+  if (!tma) return launch_quant_generic<DT, MODE>(p, s);
+  // parity views (row-major scales, 4/6 choice) get their own instantiation
+  return (p.scales_rm || p.pick4) ? launch_quant_seg<DT, MODE, true>(p, s)
+                                  : launch_quant_seg<DT, MODE, false>(p, s);
+}
+
 template <int DT>
 int dispatch_mode(const QParams& p, cudaStream_t s, bool tma) {
   switch (p.mode) {
     case F46_FIXED6:
-      return tma ? launch_quant_seg<DT, FIXED6>(p, s) : launch_quant_generic<DT, FIXED6>(p, s);
+      return launch_quant<DT, FIXED6>(p, s, tma);
     case F46_FIXED4:
-      return tma ? launch_quant_seg<DT, FIXED4>(p, s) : launch_quant_generic<DT, FIXED4>(p, s);
+      return launch_quant<DT, FIXED4>(p, s, tma);
     default:
-      return tma ? launch_quant_seg<DT, ADAPTIVE>(p, s) : launch_quant_generic<DT, ADAPTIVE>(p, s);
+      return launch_quant<DT, ADAPTIVE>(p, s, tma);
   }
 }
 
