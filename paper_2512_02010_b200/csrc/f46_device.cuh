@@ -425,23 +425,20 @@ __device__ __forceinline__ float2 bf16x2_unpack(uint32_t w) {
 }
 
 // Quotient-space squared error of one candidate,  sum_i (v_i - q_i)^2  with
-// q_i = x_i * rq (the lower-bound reciprocal) and v_i = E2M1(q_i).  Two
-// independent f32x2 accumulators; any order of the 16 f32 additions stays
-// inside the 2^-20 relative bound the decision tolerance allows for.
+// q_i = x_i * rq (the lower-bound reciprocal) and v_i = E2M1(q_i).  One f32x2
+// accumulator; any order of the 16 f32 additions stays inside the 2^-20
+// relative bound the decision tolerance allows for.
 __device__ __forceinline__ float cand_err(const float2 (&x)[8], float rq) {
   const float2 r2 = make_float2(rq, rq);
-  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+  float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const float2 q = __fmul2_rn(x[p], r2);
     const uint32_t v = e2m1x2_roundtrip(q.y, q.x);
     const float2 r = make_float2(fhadd_h<0>(v, -q.x), fhadd_h<1>(v, -q.y));
-    if (p & 1)
-      acc1 = __ffma2_rn(r, r, acc1);
-    else
-      acc0 = __ffma2_rn(r, r, acc0);
+    acc = __ffma2_rn(r, r, acc);
   }
-  return (acc0.x + acc0.y) + (acc1.x + acc1.y);
+  return acc.x + acc.y;
 }
 
 // Packed codes of x * r (16 nibbles, element i at bits [4i, 4i+4)).
@@ -564,13 +561,37 @@ __device__ __forceinline__ bool fast_block(const float2 (&x)[8], float bmax, con
 // ambiguous 4/6 decision) folds into the returned flag, so consecutive blocks
 // of one lane can be scheduled together.  Same arithmetic and bounds as
 // fast_block.
+// TDIR == 0 means alpha = amax/mcap exactly: alpha has <= 8 significant bits,
+// so D = alpha*Delta (<= 12 bits) is exact in f32, every near-tie quotient is an
+// exact tie, and non-ties stay >= 2^-16.3 (relative) away from one.  One
+// Newton step  q1 = q0 - fma(q0, D, -x) * R  (residual exact, R ~ 1/D within
+// 2^-22) lands exactly on a tie t (|q1 - t| <= t * 2^-43 before rounding) and
+// within 2^-22 of every other quotient, so cvt.rn's ties-to-even is exact.
+__device__ __forceinline__ uint64_t codes_newton(const float2 (&x)[8], float D, float R) {
+  // Written as q1 = q0 + fma(q0, D, -x) * (-R) so that x = -0.0 keeps its sign
+  // (every zero term is then -0 + -0); a +0 residual would turn q1 into +0.
+  const float2 R2 = make_float2(R, R), nR2 = make_float2(-R, -R), D2 = make_float2(D, D);
+  float2 q[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const float2 q0 = __fmul2_rn(x[p], R2);
+    const float2 e = __ffma2_rn(q0, D2, make_float2(-x[p].x, -x[p].y));
+    q[p] = __ffma2_rn(e, nR2, q0);
+  }
+  const uint32_t w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  const uint32_t w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]);
+  return ((uint64_t)w1 << 32) | w0;
+}
+
 template <int TDIR, class Load>
-__device__ __forceinline__ uint64_t codes_dir(const float2 (&x)[8], float rq, float alpha,
-                                              float delta, const Load& load) {
+__device__ __forceinline__ uint64_t codes_dir(const float2 (&x)[8], float rq, float D,
+                                              float alpha, float delta, const Load& load) {
   if constexpr (TDIR < 0) {
     return codes_of(x, rq);
   } else if constexpr (TDIR == 1) {
     return codes_of(x, rq * F46_QHI_OVER_QLO);
+  } else if constexpr (TDIR == 0) {
+    return codes_newton(x, D, rq);
   } else {
     return exact_codes(x, rq, alpha, delta, TDIR, load);
   }
@@ -590,8 +611,9 @@ __device__ __forceinline__ bool block_sl(const float2 (&x)[8], float bmax, const
     const uint32_t sc = pr & 0xFFu;
     ok &= ((pr >> 8) == sc) & (sc != 0u);
     const float delta = e4m3_to_f32(sc);
-    const float rq = rcp_approx(alpha * delta) * F46_QLO;
-    out.codes = codes_dir<TDIR>(x, rq, alpha, delta, load);
+    const float D = alpha * delta;
+    const float rq = rcp_approx(D) * F46_QLO;
+    out.codes = codes_dir<TDIR>(x, rq, D, alpha, delta, load);
     out.sc = sc;
     out.pick4 = (MODE == FIXED4);
   } else {
@@ -613,7 +635,7 @@ __device__ __forceinline__ bool block_sl(const float2 (&x)[8], float bmax, const
                            fmaf(0x1p-14f, ssum, fmaf(0x1p-32f * bmax, bmax, 0x1p-140f)));
     ok &= fabsf(s.x - s.y) > tol;  // NaN (from a rejected block) compares false
     const bool k = s.y < s.x;
-    out.codes = codes_dir<TDIR>(x, k ? rq.y : rq.x, alpha, k ? dlt.y : dlt.x, load);
+    out.codes = codes_dir<TDIR>(x, k ? rq.y : rq.x, k ? D.y : D.x, alpha, k ? dlt.y : dlt.x, load);
     out.sc = k ? (pl >> 8) : (pl & 0xFFu);
     out.pick4 = k;
   }
