@@ -1,21 +1,342 @@
-// f46_gemm.cu -- tcgen05 block-scaled NVFP4 GEMM (kind::mxf4nvf4) + C ABI.
-// (placeholder entry points until the kernel lands)
+// f46_gemm.cu -- block-scaled NVFP4 GEMM on the 5th-generation tensor cores
+// (tcgen05.mma kind::mxf4nvf4, scale_vec::4X: E2M1 operands, UE4M3 scales per
+// 16 K-elements, f32 accumulation in TMEM) + its C ABI.
+//
+//   C[M,N] = alpha_a * alpha_b * sum_k (a[m,k] * sa[m,k/16]) * (b[n,k] * sb[n,k/16])
+//
+// which is the reference's emulated_fp4_matmul(aq, bq, transpose_b=True)
+// (qlinear.py:74-93): dequantize both operands, multiply, accumulate.  Both
+// operands are f46_quantize outputs, K-major ("TN"): packed E2M1 codes
+// [rows][K/2] and E4M3 scales in the tcgen05 128x4 tile layout, so they feed
+// the tensor cores without any repacking.
+//
+// Kernel shape (one CTA per 128 x 256 output tile, 192 threads):
+//   warp 0      TMA producer: per 256-wide K step, one 128x128 B box of A codes,
+//               one 256x128 B box of B codes (128-byte swizzle) and the
+//               matching 512-byte scale-factor atoms (1-D bulk copies), into a
+//               4-stage shared-memory ring guarded by full/empty mbarriers.
+//   warp 1      TMEM allocator and MMA issuer: one elected thread copies the
+//               stage's scale factors smem -> TMEM (tcgen05.cp 32x128b.warpx4,
+//               double-buffered) and issues 4 MMAs of 128x256x64; tcgen05.commit
+//               releases the stage, and finally the accumulator.
+//   warps 2-5   epilogue: tcgen05.ld the 128x256 f32 accumulator (each warp its
+//               32-lane quadrant), scale by alpha_a*alpha_b, store f32 or bf16.
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
 
 #include "../../include/fouroversix.h"
+#include "f46_ptx.cuh"
+
+using namespace f46::ptx;
+
+namespace {
+
+constexpr int BM = 128;           // output rows per CTA (UMMA M)
+constexpr int BN = 256;           // output cols per CTA (UMMA N)
+constexpr int BK = 256;           // K elements per pipeline stage (128 bytes of E2M1)
+constexpr int UK = 64;            // K per tcgen05.mma
+constexpr int kStagesG = 4;
+constexpr int A_BYTES = BM * BK / 2;            // 16 KB
+constexpr int B_BYTES = BN * BK / 2;            // 32 KB
+constexpr int SFA_BYTES = (BM / 128) * 4 * 512; // 4 atoms of 128 rows x 4 scale blocks
+constexpr int SFB_BYTES = (BN / 128) * 4 * 512;
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + SFA_BYTES + SFB_BYTES;
+constexpr int SMEM_BYTES = kStagesG * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
+constexpr uint32_t TMEM_COLS = 512;               // 256 accumulator + 2 x 48 scale columns
+constexpr uint32_t TM_SF = 256;                   // first scale-factor column
+constexpr uint32_t TM_SF_BUF = 48;                // per buffer: 16 (SFA) + 32 (SFB)
+constexpr int kThreads = 192;
+
+// Instruction descriptor: E2M1 x E2M1 (MXF4 format 1), UE4M3 scales, f32
+// accumulation, both operands K-major, M = 128, N = 256, K = 64.
+constexpr uint32_t kIdesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+struct GemmParams {
+  const uint8_t* sfa;  // group 0 scale atoms of A
+  const uint8_t* sfb;
+  const double* alpha_a;
+  const double* alpha_b;
+  void* c;
+  int64_t M, N, K, ldc;
+  int64_t sfa_group_stride, sfb_group_stride;  // bytes
+  int64_t c_group_stride;                      // elements
+  int alpha_group_stride;                      // 0: shared alpha, 1: one per group
+  int c_bf16;
+};
+
+template <int OUT_BF16>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_nvfp4_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                      const __grid_constant__ CUtensorMap tmap_b, const GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sm_a = smem;
+  uint8_t* sm_b = sm_a + kStagesG * A_BYTES;
+  uint8_t* sm_sfa = sm_b + kStagesG * B_BYTES;
+  uint8_t* sm_sfb = sm_sfa + kStagesG * SFA_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm_sfb + kStagesG * SFB_BYTES);
+  uint64_t* empty = full + kStagesG;
+  uint64_t* acc_full = empty + kStagesG;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.z;
+  const int64_t n0 = (int64_t)blockIdx.x * BN, m0 = (int64_t)blockIdx.y * BM;
+  const int64_t nb = (p.K + 15) >> 4;          // scale blocks per row
+  const int64_t kb4 = (nb + 3) >> 2;           // 512-byte atoms per 128-row tile
+  const int ktiles = (int)((kb4 + 3) >> 2);    // pipeline steps (4 atoms = 256 K each)
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+    for (int s = 0; s < kStagesG; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  // Scale atoms that a partial tile leaves unloaded are read by nobody, but the
+  // B tile's second 128-row atom may be absent (N <= n0 + 128): zero the
+  // scale-factor ring once so a stale byte can never be a NaN code.
+  for (int i = threadIdx.x; i < kStagesG * (SFA_BYTES + SFB_BYTES) / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sm_sfa)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 1) tmem_alloc(tmem_holder, TMEM_COLS);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint8_t* sfa = p.sfa + g * p.sfa_group_stride + ((m0 >> 7) * kb4) * 512;
+      const uint8_t* sfb0 = p.sfb + g * p.sfb_group_stride + ((n0 >> 7) * kb4) * 512;
+      const bool b_hi = ((n0 >> 7) + 1) < ((p.N + 127) >> 7);  // second 128-row atom exists
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStagesG;
+        if (kt >= kStagesG) mbar_wait(&empty[s], ((kt / kStagesG) - 1) & 1);
+        const int natoms = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
+        const uint32_t sfbytes = natoms * 512;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES + sfbytes * (b_hi ? 3 : 2));
+        tma_load_3d(smem_u32(sm_a + s * A_BYTES), &tmap_a, &full[s], kt * (BK / 2), (int)m0, g);
+        tma_load_3d(smem_u32(sm_b + s * B_BYTES), &tmap_b, &full[s], kt * (BK / 2), (int)n0, g);
+        bulk_load(smem_u32(sm_sfa + s * SFA_BYTES), sfa + (int64_t)kt * 2048, sfbytes, &full[s]);
+        bulk_load(smem_u32(sm_sfb + s * SFB_BYTES), sfb0 + (int64_t)kt * 2048, sfbytes, &full[s]);
+        if (b_hi)
+          bulk_load(smem_u32(sm_sfb + s * SFB_BYTES + 2048), sfb0 + kb4 * 512 + (int64_t)kt * 2048,
+                    sfbytes, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStagesG;
+        mbar_wait(&full[s], (kt / kStagesG) & 1);
+        tc_fence_after();
+        const int nk = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
+        const uint32_t tsfa = tmem + TM_SF + (kt & 1) * TM_SF_BUF;
+        const uint32_t tsfb = tsfa + 16;
+        const uint32_t a_addr = smem_u32(sm_a + s * A_BYTES);
+        const uint32_t b_addr = smem_u32(sm_b + s * B_BYTES);
+        const uint32_t sfa_addr = smem_u32(sm_sfa + s * SFA_BYTES);
+        const uint32_t sfb_addr = smem_u32(sm_sfb + s * SFB_BYTES);
+        for (int j = 0; j < nk; ++j) {
+          // one 512-byte atom = 32 rows x 16 bytes (8-row core matrices 128 B apart)
+          tc_cp_32x128b_x4(tsfa + 4 * j, smem_desc(sfa_addr + 512 * j, 0, 128, 0));
+          tc_cp_32x128b_x4(tsfb + 8 * j, smem_desc(sfb_addr + 512 * j, 0, 128, 0));
+          tc_cp_32x128b_x4(tsfb + 8 * j + 4, smem_desc(sfb_addr + 2048 + 512 * j, 0, 128, 0));
+        }
+        for (int j = 0; j < nk; ++j) {
+          // K-major, 128-byte swizzle: rows 128 B apart, 8-row groups 1024 B apart;
+          // the K offset of step j is 32 bytes inside the swizzle atom.
+          const uint64_t ad = smem_desc(a_addr + 32 * j, 16, 1024, 2);
+          const uint64_t bd = smem_desc(b_addr + 32 * j, 16, 1024, 2);
+          mma_nvf4(tmem, ad, bd, kIdesc, (kt | j) != 0, tsfa + 4 * j, tsfb + 8 * j);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(acc_full);
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const float alpha = (float)(p.alpha_a[g * p.alpha_group_stride] *
+                                p.alpha_b[g * p.alpha_group_stride]);
+    const int64_t row = m0 + 32 * q + lane;
+    const bool row_ok = row < p.M;
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tc_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + 32 * c, r);
+      tc_wait_ld();
+      const int64_t col0 = n0 + 32 * c;
+      if (!row_ok || col0 >= p.N) continue;
+      if (OUT_BF16) {
+        __nv_bfloat16* out =
+            reinterpret_cast<__nv_bfloat16*>(p.c) + g * p.c_group_stride + row * p.ldc + col0;
+        if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 v;
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(r[i]) * alpha,
+                                                      __uint_as_float(r[i + 1]) * alpha);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(r[i + 2]) * alpha,
+                                                      __uint_as_float(r[i + 3]) * alpha);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[i + 4]) * alpha,
+                                                      __uint_as_float(r[i + 5]) * alpha);
+            __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(r[i + 6]) * alpha,
+                                                      __uint_as_float(r[i + 7]) * alpha);
+            v.x = *reinterpret_cast<uint32_t*>(&h0);
+            v.y = *reinterpret_cast<uint32_t*>(&h1);
+            v.z = *reinterpret_cast<uint32_t*>(&h2);
+            v.w = *reinterpret_cast<uint32_t*>(&h3);
+            *reinterpret_cast<uint4*>(out + i) = v;
+          }
+        } else {
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < p.N) out[i] = __float2bfloat16_rn(__uint_as_float(r[i]) * alpha);
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(p.c) + g * p.c_group_stride + row * p.ldc + col0;
+        if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<float4*>(out + i) =
+                make_float4(__uint_as_float(r[i]) * alpha, __uint_as_float(r[i + 1]) * alpha,
+                            __uint_as_float(r[i + 2]) * alpha, __uint_as_float(r[i + 3]) * alpha);
+        } else {
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < p.N) out[i] = __uint_as_float(r[i]) * alpha;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// 3-D map over packed codes [groups][rows][kbytes] (uint8), box kbytes 128 x box_rows.
+bool make_code_map(CUtensorMap* m, const uint8_t* codes, int64_t groups, int64_t rows,
+                   int64_t kbytes, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)kbytes, (cuuint64_t)rows, (cuuint64_t)groups};
+  const cuuint64_t strides[2] = {(cuuint64_t)kbytes, (cuuint64_t)(kbytes * rows)};
+  const cuuint32_t box[3] = {128, box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(codes), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const double* alpha_a,
+                const uint8_t* b_codes, const uint8_t* b_sf, const double* alpha_b, int64_t M,
+                int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype, int alpha_per_group,
+                cudaStream_t stream) {
+  if (!a_codes || !a_sf || !alpha_a || !b_codes || !b_sf || !alpha_b || !c) return F46_ERR_INVALID_ARG;
+  if (groups < 1 || M <= 0 || N <= 0 || K <= 0 || ldc < N) return F46_ERR_INVALID_ARG;
+  if (c_dtype != F46_DT_F32 && c_dtype != F46_DT_BF16) return F46_ERR_INVALID_ARG;
+  const int64_t nb = (K + 15) / 16;
+  const int64_t kbytes = nb * 8;
+  // TMA row pitch must be a multiple of 16 bytes; tile coordinates are int32
+  if (kbytes % 16 != 0 || M >= (1ll << 31) || N >= (1ll << 31)) return F46_ERR_UNSUPPORTED;
+  if ((((uintptr_t)a_codes) | ((uintptr_t)b_codes)) & 15) return F46_ERR_UNSUPPORTED;
+  if ((((uintptr_t)a_sf) | ((uintptr_t)b_sf)) & 15) return F46_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb;
+  if (!make_code_map(&ma, a_codes, groups, M, kbytes, BM) ||
+      !make_code_map(&mb, b_codes, groups, N, kbytes, BN))
+    return F46_ERR_CUDA;
+  GemmParams p;
+  p.sfa = a_sf;
+  p.sfb = b_sf;
+  p.alpha_a = alpha_a;
+  p.alpha_b = alpha_b;
+  p.c = c;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.ldc = ldc;
+  p.sfa_group_stride = (int64_t)f46_scales_tc_bytes(M, K);
+  p.sfb_group_stride = (int64_t)f46_scales_tc_bytes(N, K);
+  p.c_group_stride = M * ldc;
+  p.alpha_group_stride = alpha_per_group ? 1 : 0;
+  p.c_bf16 = c_dtype == F46_DT_BF16;
+  const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)groups);
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(gemm_nvfp4_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_nvfp4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
+  });
+  if (p.c_bf16)
+    gemm_nvfp4_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ma, mb, p);
+  else
+    gemm_nvfp4_kernel<0><<<grid, kThreads, SMEM_BYTES, stream>>>(ma, mb, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[fouroversix] gemm launch: %s\n", cudaGetErrorString(e));
+    return F46_ERR_CUDA;
+  }
+  return F46_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
-int f46_gemm_nvfp4(const uint8_t*, const uint8_t*, const double*, const uint8_t*, const uint8_t*,
-                   const double*, int64_t, int64_t, int64_t, void*, int64_t, int, f46_stream_t) {
-  return F46_ERR_UNSUPPORTED;
+int f46_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_scales_tc, const double* d_alpha_a,
+                   const uint8_t* b_codes, const uint8_t* b_scales_tc, const double* d_alpha_b,
+                   int64_t M, int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                   f46_stream_t stream) {
+  return gemm_launch(1, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M, N, K,
+                     c, ldc, c_dtype, 0, (cudaStream_t)stream);
 }
 
-int f46_gemm_nvfp4_grouped(int, const uint8_t*, const uint8_t*, const double*, const uint8_t*,
-                           const uint8_t*, const double*, int64_t, int64_t, int64_t, void*,
-                           int64_t, int, f46_stream_t) {
-  return F46_ERR_UNSUPPORTED;
+int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
+                           const double* d_alpha_a, const uint8_t* b_codes,
+                           const uint8_t* b_scales_tc, const double* d_alpha_b, int64_t M,
+                           int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                           f46_stream_t stream) {
+  return gemm_launch(groups, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M,
+                     N, K, c, ldc, c_dtype, 1, (cudaStream_t)stream);
 }
 
 int f46_quantize_2d(const void*, int, int64_t, int64_t, int, int, double, const double*, double,

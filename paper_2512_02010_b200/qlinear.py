@@ -1,0 +1,98 @@
+"""NVFP4 GEMM consumer of the quantized containers.
+
+Mirrors the reference's fp4emu.qlinear (/root/reference/pkg/src/fp4emu/
+qlinear.py): ``emulated_fp4_matmul`` (:74-93) and ``round_to_bf16`` (:56-61).
+
+``emulated_fp4_matmul(aq, bq, transpose_b=True)`` -- both operands blocked
+along K, the layout of every NVFP4 linear layer (FPROP x @ W^T, WGRAD) -- runs
+on the B200's tensor cores: ``f46_gemm_nvfp4`` issues tcgen05.mma
+kind::mxf4nvf4 directly on the packed E2M1 codes and the tcgen05-layout E4M3
+scales the quantizer wrote, with alpha_a * alpha_b applied in the epilogue.
+The reference dequantizes to float32 and accumulates in float32 in ascending
+k; the tensor cores accumulate the same exact products in float32 in their own
+order, so results agree to float32 accumulation error (relative Frobenius
+<= 1e-5, the reference's own bound, test_acceptance.py:191-198).
+
+``transpose_b=False`` asks for dequant(A) @ dequant(B) with B blocked along N,
+which no block-scaled tensor-core instruction can consume; that case
+dequantizes both operands exactly on the GPU (f46_dequantize) and multiplies
+in float32 with TF32 disabled.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .blockquant import QuantizedTensor, _stream, dequantize_tensor
+from .errors import InvalidInputError
+
+__all__ = ["emulated_fp4_matmul", "gemm_nvfp4", "gemm_nvfp4_grouped", "round_to_bf16"]
+
+
+def round_to_bf16(x: torch.Tensor) -> torch.Tensor:
+    """float32 -> bf16 -> float32, round to nearest even (qlinear.py:56-61)."""
+    return x.to(torch.float32).to(torch.bfloat16).to(torch.float32)
+
+
+def gemm_nvfp4(aq: QuantizedTensor, bq: QuantizedTensor, out_dtype=torch.float32,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """C[M,N] = dequant(aq) @ dequant(bq)^T on tcgen05 (both blocked along K)."""
+    L = _lib.load()
+    if len(aq.shape) != 2 or len(bq.shape) != 2:
+        raise InvalidInputError("the NVFP4 GEMM is defined for 2-D operands")
+    M, K = aq.shape
+    N, Kb = bq.shape
+    if K != Kb:
+        raise InvalidInputError(f"inner dimensions differ: {aq.shape} x {tuple(bq.shape)}^T")
+    dev = aq.scales_tc.device
+    dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16}[out_dtype]
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=dev)
+    rc = L.f46_gemm_nvfp4(aq.packed_codes.data_ptr(), aq.scales_tc.data_ptr(),
+                          aq.alpha_dev.data_ptr(), bq.packed_codes.data_ptr(),
+                          bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, K,
+                          out.data_ptr(), out.stride(0), dt, _stream())
+    _lib.check(rc, "f46_gemm_nvfp4")
+    return out
+
+
+def gemm_nvfp4_grouped(a_codes, a_scales, a_alpha, b_codes, b_scales, b_alpha, M, N, K,
+                       out_dtype=torch.float32) -> torch.Tensor:
+    """G independent GEMMs of one shape (MoE experts): operands packed back to
+    back ([G, ...] device tensors), one alpha per group, C is [G, M, N]."""
+    L = _lib.load()
+    G = a_codes.shape[0]
+    dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16}[out_dtype]
+    out = torch.empty((G, M, N), dtype=out_dtype, device=a_codes.device)
+    rc = L.f46_gemm_nvfp4_grouped(G, a_codes.data_ptr(), a_scales.data_ptr(), a_alpha.data_ptr(),
+                                  b_codes.data_ptr(), b_scales.data_ptr(), b_alpha.data_ptr(),
+                                  M, N, K, out.data_ptr(), N, dt, _stream())
+    _lib.check(rc, "f46_gemm_nvfp4_grouped")
+    return out
+
+
+def emulated_fp4_matmul(aq: QuantizedTensor, bq: QuantizedTensor, *, transpose_b: bool = False,
+                        bf16_out: bool = False) -> torch.Tensor:
+    """matmul(dequantize(aq), dequantize(bq)) with 32-bit accumulation
+    (qlinear.py:74-93).  Returns a float32 CUDA tensor (bf16-rounded values
+    when ``bf16_out``)."""
+    if len(aq.shape) != 2 or len(bq.shape) != 2:
+        raise InvalidInputError("emulated matmul is defined for 2-D operands")
+    if transpose_b:
+        if aq.shape[1] != bq.shape[1]:
+            raise InvalidInputError(f"inner dimensions differ: {aq.shape} x {tuple(bq.shape[::-1])}")
+        if bf16_out:
+            return gemm_nvfp4(aq, bq, torch.bfloat16).to(torch.float32)
+        return gemm_nvfp4(aq, bq, torch.float32)
+    if aq.shape[1] != bq.shape[0]:
+        raise InvalidInputError(f"inner dimensions differ: {aq.shape} x {bq.shape}")
+    A = dequantize_tensor(aq, torch.float32)
+    B = dequantize_tensor(bq, torch.float32)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        C = A @ B
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return round_to_bf16(C) if bf16_out else C
