@@ -27,6 +27,9 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <stdlib.h>
+
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/fouroversix.h"
@@ -231,6 +234,227 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent variant: one CTA per SM walks a grouped raster of output tiles.
+// The producer runs ahead across tile boundaries (the next tile's operands
+// stream in while the current tile drains), and the single TMEM accumulator is
+// handed back to the MMA warp (acc_empty) as soon as the eight epilogue warps
+// have pulled it into registers (128 f32 columns per thread); scaling,
+// conversion and the global stores then overlap the next tile's MMAs.
+// ---------------------------------------------------------------------------
+#ifndef F46_GEMM_DEBUG
+#define F46_GEMM_DEBUG 0
+#endif
+constexpr int kStagesP = 4;
+constexpr int SMEM_BYTES_P = kStagesP * STAGE_BYTES + 1024 + 1024;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, 128 columns each
+constexpr int kThreadsP = 64 + 32 * kEpiWarps;
+constexpr int kGroupM = 16;  // raster band height (m-tiles) for L2 reuse
+
+struct TileCoord {
+  int g, mt, nt;
+};
+
+__device__ __forceinline__ TileCoord tile_of(int t, int num_m, int num_n) {
+  const int per_g = num_m * num_n;
+  TileCoord c;
+  c.g = t / per_g;
+  const int r = t - c.g * per_g;
+  const int band = r / (kGroupM * num_n);
+  const int idx = r - band * (kGroupM * num_n);
+  const int rows = min(kGroupM, num_m - band * kGroupM);
+  c.mt = band * kGroupM + idx % rows;
+  c.nt = idx / rows;
+  return c;
+}
+
+template <int OUT_BF16>
+__global__ void __launch_bounds__(kThreadsP, 1)
+    gemm_nvfp4_persistent(const __grid_constant__ CUtensorMap tmap_a,
+                          const __grid_constant__ CUtensorMap tmap_b, const GemmParams p,
+                          int groups) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sm_a = smem;
+  uint8_t* sm_b = sm_a + kStagesP * A_BYTES;
+  uint8_t* sm_sfa = sm_b + kStagesP * B_BYTES;
+  uint8_t* sm_sfb = sm_sfa + kStagesP * SFA_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm_sfb + kStagesP * SFB_BYTES);
+  uint64_t* empty = full + kStagesP;
+  uint64_t* acc_full = empty + kStagesP;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nb = (p.K + 15) >> 4;
+  const int64_t kb4 = (nb + 3) >> 2;
+  const int ktiles = (int)((kb4 + 3) >> 2);
+  const int num_m = (int)((p.M + BM - 1) / BM), num_n = (int)((p.N + BN - 1) / BN);
+  const int num_tiles = groups * num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+    for (int s = 0; s < kStagesP; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kEpiWarps);
+    fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < kStagesP * (SFA_BYTES + SFB_BYTES) / 16; i += kThreadsP)
+    reinterpret_cast<uint4*>(sm_sfa)[i] = make_uint4(0, 0, 0, 0);
+  if (warp == 1) tmem_alloc(tmem_holder, TMEM_COLS);
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const TileCoord tc = tile_of(t, num_m, num_n);
+        const int64_t m0 = (int64_t)tc.mt * BM, n0 = (int64_t)tc.nt * BN;
+        const uint8_t* sfa = p.sfa + tc.g * p.sfa_group_stride + ((m0 >> 7) * kb4) * 512;
+        const uint8_t* sfb0 = p.sfb + tc.g * p.sfb_group_stride + ((n0 >> 7) * kb4) * 512;
+        const bool b_hi = ((n0 >> 7) + 1) < ((p.N + 127) >> 7);
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStagesP;
+          if (it >= kStagesP) mbar_wait(&empty[s], ((it / kStagesP) - 1) & 1);
+          const int natoms = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
+          const uint32_t sfbytes = natoms * 512;
+#if F46_GEMM_DEBUG == 1
+          mbar_arrive(&full[s]);  // debug: no operand traffic
+          continue;
+#endif
+          mbar_expect_tx(&full[s], A_BYTES + B_BYTES + sfbytes * (b_hi ? 3 : 2));
+          tma_load_3d(smem_u32(sm_a + s * A_BYTES), &tmap_a, &full[s], kt * (BK / 2), (int)m0, tc.g);
+          tma_load_3d(smem_u32(sm_b + s * B_BYTES), &tmap_b, &full[s], kt * (BK / 2), (int)n0, tc.g);
+          bulk_load(smem_u32(sm_sfa + s * SFA_BYTES), sfa + (int64_t)kt * 2048, sfbytes, &full[s]);
+          bulk_load(smem_u32(sm_sfb + s * SFB_BYTES), sfb0 + (int64_t)kt * 2048, sfbytes, &full[s]);
+          if (b_hi)
+            bulk_load(smem_u32(sm_sfb + s * SFB_BYTES + 2048),
+                      sfb0 + kb4 * 512 + (int64_t)kt * 2048, sfbytes, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+        if (lt > 0) {
+          mbar_wait(acc_empty, (lt - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStagesP;
+          mbar_wait(&full[s], (it / kStagesP) & 1);
+          tc_fence_after();
+          const int nk = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
+          const uint32_t tsfa = tmem + TM_SF + (it & 1) * TM_SF_BUF;
+          const uint32_t tsfb = tsfa + 16;
+          const uint32_t a_addr = smem_u32(sm_a + s * A_BYTES);
+          const uint32_t b_addr = smem_u32(sm_b + s * B_BYTES);
+          const uint32_t sfa_addr = smem_u32(sm_sfa + s * SFA_BYTES);
+          const uint32_t sfb_addr = smem_u32(sm_sfb + s * SFB_BYTES);
+#if F46_GEMM_DEBUG != 3 && F46_GEMM_DEBUG != 4
+          for (int j = 0; j < nk; ++j) {
+            tc_cp_32x128b_x4(tsfa + 4 * j, smem_desc(sfa_addr + 512 * j, 0, 128, 0));
+            tc_cp_32x128b_x4(tsfb + 8 * j, smem_desc(sfb_addr + 512 * j, 0, 128, 0));
+            tc_cp_32x128b_x4(tsfb + 8 * j + 4, smem_desc(sfb_addr + 2048 + 512 * j, 0, 128, 0));
+          }
+#endif
+#if F46_GEMM_DEBUG != 2 && F46_GEMM_DEBUG != 4
+          for (int j = 0; j < nk; ++j) {
+            const uint64_t ad = smem_desc(a_addr + 32 * j, 16, 1024, 2);
+            const uint64_t bd = smem_desc(b_addr + 32 * j, 16, 1024, 2);
+            mma_nvf4(tmem, ad, bd, kIdesc, (kt | j) != 0, tsfa + 4 * j, tsfb + 8 * j);
+          }
+#endif
+          tc_commit(&empty[s]);
+        }
+        tc_commit(acc_full);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;              // TMEM lane quadrant this warp may access
+    const int h = (warp - 2) >> 2;       // column half
+    const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + 128 * h;
+    int lt = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++lt) {
+      const TileCoord tc = tile_of(t, num_m, num_n);
+      const float alpha = (float)(p.alpha_a[tc.g * p.alpha_group_stride] *
+                                  p.alpha_b[tc.g * p.alpha_group_stride]);
+      mbar_wait(acc_full, lt & 1);
+      tc_fence_after();
+#if F46_GEMM_DEBUG == 5
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      continue;
+#endif
+      uint32_t r[4][32];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc_ld_32x32b_x32(taddr + 32 * i, r[i]);
+      tc_wait_ld();
+      // the accumulator is in registers: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+      const int64_t row = (int64_t)tc.mt * BM + 32 * q + lane;
+      if (row >= p.M) continue;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t col0 = (int64_t)tc.nt * BN + 128 * h + 32 * i;
+        if (col0 >= p.N) break;
+        if (OUT_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + tc.g * p.c_group_stride +
+                               row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[i][j + 2 * k]) * alpha,
+                                                         __uint_as_float(r[i][j + 2 * k + 1]) * alpha);
+                w[k] = *reinterpret_cast<uint32_t*>(&v);
+              }
+              *reinterpret_cast<uint4*>(out + j) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+              out[j] = __float2bfloat16_rn(__uint_as_float(r[i][j]) * alpha);
+          }
+        } else {
+          float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(out + j) = make_float4(
+                  __uint_as_float(r[i][j]) * alpha, __uint_as_float(r[i][j + 1]) * alpha,
+                  __uint_as_float(r[i][j + 2]) * alpha, __uint_as_float(r[i][j + 3]) * alpha);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = __uint_as_float(r[i][j]) * alpha;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -298,6 +522,35 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   p.c_group_stride = M * ldc;
   p.alpha_group_stride = alpha_per_group ? 1 : 0;
   p.c_bf16 = c_dtype == F46_DT_BF16;
+  // Persistent kernel unless F46_GEMM_SIMPLE asks for the one-tile-per-CTA one.
+  if (!getenv("F46_GEMM_SIMPLE")) {
+    static std::once_flag pattr_once;
+    std::call_once(pattr_once, [] {
+      cudaFuncSetAttribute(gemm_nvfp4_persistent<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES_P);
+      cudaFuncSetAttribute(gemm_nvfp4_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES_P);
+    });
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (sms <= 0) sms = 148;
+    }
+    const int64_t tiles = (int64_t)groups * ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    if (p.c_bf16)
+      gemm_nvfp4_persistent<1><<<grid, kThreadsP, SMEM_BYTES_P, stream>>>(ma, mb, p, groups);
+    else
+      gemm_nvfp4_persistent<0><<<grid, kThreadsP, SMEM_BYTES_P, stream>>>(ma, mb, p, groups);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[fouroversix] gemm launch: %s\n", cudaGetErrorString(e));
+      return F46_ERR_CUDA;
+    }
+    return F46_OK;
+  }
   const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)groups);
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {

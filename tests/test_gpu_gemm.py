@@ -143,3 +143,20 @@ def test_grouped_matches_per_group():
                                  torch.cat([q.alpha_dev for q in qb]), M, N, K)
     for i in range(G):
         assert torch.equal(out[i], f46.gemm_nvfp4(qa[i], qb[i]))
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
+    """The persistent kernel and the one-tile-per-CTA kernel (F46_GEMM_SIMPLE)
+    accumulate every tile in the same order: identical bits, also into a
+    strided output (ldc = N + 1)."""
+    M, N, K = 700, 1000, 1024
+    aq = f46.quantize_tensor_adaptive(bf16_randn((M, K), 71).cuda(), ADAPT)
+    bq = f46.quantize_tensor_adaptive(bf16_randn((N, K), 72).cuda(), ADAPT)
+    fast = f46.gemm_nvfp4(aq, bq, out_dtype)
+    wide = torch.empty((M, N + 1), dtype=out_dtype, device="cuda")
+    strided = f46.gemm_nvfp4(aq, bq, out_dtype, out=wide[:, :N])
+    monkeypatch.setenv("F46_GEMM_SIMPLE", "1")
+    simple = f46.gemm_nvfp4(aq, bq, out_dtype)
+    assert torch.equal(fast, simple) and torch.equal(fast, strided)
+    assert rel_fro(fast.float(), gpu_oracle(aq, bq)) <= (REL_TOL if out_dtype == torch.float32 else 4e-3)
