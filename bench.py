@@ -1,21 +1,22 @@
-"""Benchmark of the B200-native 4/6 NVFP4 quantization path (driver contract).
+"""Benchmark of the B200-native 4/6 NVFP4 path (driver contract).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-Workload (config.workload): BASELINE.json config 3 -- end-to-end 4/6
-quantization (amax -> allreduce(MAX) -> fused adaptive quantize) of a
-65536 x 4096 BF16 activation tensor, row-sharded over the N ranks (strong
-scaling; N=1 holds the whole tensor).  One step = one pass over the tensor.
-Metric: GB/s of algorithmic bytes = 4.5625 B/element (amax reads 2 B,
-quantize reads 2 B and writes 0.5 B of E2M1 codes + 1/16 B of E4M3 scales),
-whole job, max over ranks.  The 512 MB input exceeds the 126 MB L2 and L2 is
-additionally flushed before every timed step.
+Headline workload (config.workload, BASELINE.json config 3): end-to-end 4/6
+quantization -- amax (K1) -> NCCL allreduce(MAX) -> fused adaptive quantize
+(K2) -- of one 65536 x 4096 BF16 activation tensor, row-sharded over the N
+ranks (strong scaling; N = 1 holds the whole tensor).  One step = one pass
+over the tensor.  Metric: GB/s of algorithmic bytes, 4.5625 B/element (amax
+reads 2 B; quantize reads 2 B and writes 0.5 B of E2M1 codes + 1/16 B of E4M3
+scales), whole job, max over ranks.  The 512 MB input exceeds the 126 MB L2
+and L2 is also flushed (256 MB write) before every timed step.
 
-Extra objects at N=1: `roofline` for the dominant kernel (the fused 4/6
-quantize, K2) measured live with CUDA events on its stream; `cpu_baseline`
-(the CPU oracle port timed on this host on a bounded sample); `weights`
-(config 2, Llama-3-8B weight shapes); `gemm` (config 4, tcgen05 NVFP4 GEMM
-8192^3) when the GEMM is built.
+Extra objects on the N = 1 line: `roofline` of the dominant kernel (K2, CUDA
+events on its stream), `e2e` (public API, pinned host buffers, H2D + D2H
+inside the timed region), `cpu_baseline` (the CPU oracle port on a bounded
+sample), `weights` (config 2), `gemm` (config 4: tcgen05 NVFP4 GEMM 8192^3,
+its own roofline vs the FP4 tensor peak) and `moe` (config 5: Nemotron-3-Nano
+expert GEMMs, 16 experts per GPU, grouped).
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle port in oracle/, float64, all host threads) on a bounded sample of the
@@ -38,9 +39,11 @@ sys.path.insert(0, ROOT)
 
 ROWS, COLS = 65536, 4096
 BYTES_PER_ELEM = 4.5625          # end to end: amax 2 + quantize 2 + 0.5 + 1/16
-K2_BYTES_PER_ELEM = 2.5625       # fused quantize alone
+K2_BYTES_PER_ELEM = 2.5625       # fused quantize alone (BF16 in)
 METRIC = "4/6 quantize GB/s vs HBM peak; 4/6-NVFP4 GEMM TFLOPS vs FP4 tensor peak"
-WORKLOAD = "c3: 4/6 NVFP4 quantize (amax+allreduce MAX+fused adaptive quantize) of a 65536x4096 BF16 activation, row-sharded"
+WORKLOAD = ("c3: 4/6 NVFP4 quantize (amax + allreduce MAX + fused adaptive quantize) of a "
+            "65536x4096 BF16 activation, row-sharded")
+FP4_DENSE_NOMINAL_TFLOPS = 9000.0  # B200 dense FP4 (B200_PROFILING.md nominal table)
 
 
 def measured_peaks():
@@ -49,17 +52,18 @@ def measured_peaks():
         with open(p) as f:
             d = json.load(f)
         return d, "measured"
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
 def profile_traffic(kernel: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu capture, or None."""
+    """Per-launch DRAM bytes (read + write) of `kernel` from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(kernel)
+    v = d.get(kernel)
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
 
 
 class ClockSampler:
@@ -80,15 +84,16 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.2)
         except Exception:
             self.proc = None
 
     def stop(self):
         if self.proc is None:
             return None
-        time.sleep(0.25)
+        time.sleep(0.15)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -157,9 +162,10 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     gbs = elems * BYTES_PER_ELEM / sec / 1e9
-    sample = f"{sample_rows}x{COLS} BF16 rows of the c3 tensor per step (oracle port, float64, {cores} threads)"
+    sample = (f"{sample_rows}x{COLS} BF16 rows of the c3 tensor per step (oracle port: float64 C "
+              f"restatement of the reference, {cores} OpenMP threads)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": WORKLOAD, "sample_rows": sample_rows, "cols": COLS},
@@ -174,14 +180,19 @@ def run_reference(args):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+def _events(n):
+    import torch
+    return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+
 def run_b200(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2512_02010_b200 as f46
     from paper_2512_02010_b200 import _lib
-    from paper_2512_02010_b200.blockquant import amax_device, quantize_1d
+    from paper_2512_02010_b200.blockquant import amax_device, scales_tc_bytes
+    from paper_2512_02010_b200.sharded import shard_rows
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -191,7 +202,8 @@ def run_b200(args):
     L = _lib.load()
     peaks, peaks_kind = measured_peaks()
 
-    rows_local = ROWS // world
+    r0, r1 = shard_rows(ROWS, world, rank)
+    rows_local = r1 - r0
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(rows_local, COLS, generator=g, device=dev).to(torch.bfloat16)
     elems_local = x.numel()
@@ -200,26 +212,25 @@ def run_b200(args):
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     codes = torch.empty((rows_local, COLS // 2), dtype=torch.uint8, device=dev)
-    scales = torch.empty(f46.blockquant.scales_tc_bytes(rows_local, COLS), dtype=torch.uint8, device=dev)
+    scales = torch.empty(scales_tc_bytes(rows_local, COLS), dtype=torch.uint8, device=dev)
     amax = torch.zeros(1, dtype=torch.float64, device=dev)
     alpha = torch.empty(1, dtype=torch.float64, device=dev)
-    k2_start = torch.cuda.Event(enable_timing=True)
-    k2_end = torch.cuda.Event(enable_timing=True)
+    k2_s, k2_e = _events(args.steps), _events(args.steps)
 
-    def step(time_k2=False):
+    def step(i=None):
         amax.zero_()
         _lib.check(L.f46_amax(x.data_ptr(), _lib.DT_BF16, elems_local, amax.data_ptr(),
                               stream.cuda_stream), "amax")
         if world > 1:
             dist.all_reduce(amax, op=dist.ReduceOp.MAX)
-        if time_k2:
-            k2_start.record(stream)
+        if i is not None:
+            k2_s[i].record(stream)
         _lib.check(L.f46_quantize(x.data_ptr(), _lib.DT_BF16, rows_local, COLS, _lib.ADAPTIVE,
                                   0, 1536.0, amax.data_ptr(), 0.0, codes.data_ptr(),
                                   scales.data_ptr(), None, None, alpha.data_ptr(), None,
                                   stream.cuda_stream), "quantize")
-        if time_k2:
-            k2_end.record(stream)
+        if i is not None:
+            k2_e[i].record(stream)
 
     def barrier():
         torch.cuda.synchronize()
@@ -227,7 +238,8 @@ def run_b200(args):
             dist.barrier()
             torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3)):
+    warmup = max(args.warmup, 3)
+    for _ in range(warmup):
         flush_buf.fill_(1)
         step()
     barrier()
@@ -235,38 +247,34 @@ def run_b200(args):
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k2_ms = []
+    starts, ends = _events(args.steps), _events(args.steps)
     barrier()
     for i in range(args.steps):
         flush_buf.fill_(i & 0xFF)  # evict L2 (256 MB > 126 MB) outside the timed span
         starts[i].record(stream)
-        step(time_k2=True)
+        step(i)
         ends[i].record(stream)
-        torch.cuda.synchronize()
-        k2_ms.append(k2_start.elapsed_time(k2_end))
     barrier()
     clocks = sampler.stop() if rank == 0 else None
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_local = sum(step_ms) / len(step_ms)
-    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(step_ms) / len(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = elems_total * BYTES_PER_ELEM / (ms * 1e-3) / 1e9
 
     # roofline of K2 (fused quantize): algorithmic bytes / mean launch time
-    k2 = sum(k2_ms) / len(k2_ms)
-    k2_achieved = elems_local * K2_BYTES_PER_ELEM / (k2 * 1e-3) / 1e9
-    traffic = profile_traffic("quant_tma_kernel")
-    roofline = {"bound": "hbm", "kernel": "quant_tma_kernel<bf16,adaptive>", "achieved": k2_achieved,
-                "peak": peaks["hbm_gbs"], "peak_kind": peaks_kind, "unit": "GB/s",
-                "frac": k2_achieved / peaks["hbm_gbs"], "traffic": traffic,
-                "algorithmic_bytes_per_launch": elems_local * K2_BYTES_PER_ELEM,
-                "launch_ms": k2}
+    k2 = sum(s.elapsed_time(e) for s, e in zip(k2_s, k2_e)) / args.steps
+    k2_bytes = elems_local * K2_BYTES_PER_ELEM
+    k2_achieved = k2_bytes / (k2 * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "quant_seg_kernel<bf16,adaptive> (K2)",
+                "achieved": k2_achieved, "peak": peaks["hbm_gbs"], "peak_kind": peaks_kind,
+                "unit": "GB/s", "frac": k2_achieved / peaks["hbm_gbs"],
+                "traffic": profile_traffic("quant_seg_kernel"),
+                "algorithmic_bytes_per_launch": k2_bytes, "launch_ms": k2,
+                "amax_k1_ms": ms - k2}
 
-    # end to end through the public API with host buffers (pinned), N ranks
+    # end to end through the public API with pinned host buffers, N ranks
     xh = x.cpu().pin_memory()
     codes_h = torch.empty(codes.shape, dtype=torch.uint8).pin_memory()
     scales_h = torch.empty(scales.shape, dtype=torch.uint8).pin_memory()
@@ -284,8 +292,7 @@ def run_b200(args):
     for _ in range(2):
         e2e_step()
     barrier()
-    e_s = torch.cuda.Event(enable_timing=True)
-    e_e = torch.cuda.Event(enable_timing=True)
+    e_s, e_e = _events(1)[0], _events(1)[0]
     ne = max(2, min(args.steps, 5))
     e_s.record(stream)
     for _ in range(ne):
@@ -298,15 +305,16 @@ def run_b200(args):
     e2e = {"value": elems_total * BYTES_PER_ELEM / (float(te.item()) * 1e-3) / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": int(xh.numel() * 2),
            "d2h_bytes_per_step": int(codes_h.numel() + scales_h.numel()),
-           "ms_per_step": float(te.item()), "path": "quantize_tensor_adaptive (public API), pinned host buffers"}
+           "ms_per_step": float(te.item()),
+           "path": "quantize_tensor_adaptive (public API) from pinned host memory, codes+scales back"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (torch.randn N(0,1) -> bf16)",
-        "config": {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "mode": "adaptive",
-                   "parallelism": f"row-shard x{world} + NCCL allreduce(MAX)",
+        "config": {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "rows_per_rank": rows_local,
+                   "mode": "adaptive", "parallelism": f"row-shard x{world} + NCCL allreduce(MAX)",
                    "l2": "flushed (256 MB write) before every timed step; input 512 MB > L2",
                    "bytes_per_elem": BYTES_PER_ELEM},
         "roofline": roofline, "e2e": e2e,
@@ -315,10 +323,9 @@ def run_b200(args):
     }
     if rank == 0 and world == 1 and not args.no_extras:
         line["weights"] = bench_weights(args, L, dev, peaks)
+        line["gemm"] = bench_gemm(args, dev, peaks)
+        line["moe"] = bench_moe(args, dev)
         line["cpu_baseline"] = cpu_baseline(args)
-        gemm = bench_gemm(args, dev, peaks)
-        if gemm is not None:
-            line["gemm"] = gemm
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -330,18 +337,17 @@ def bench_weights(args, L, dev, peaks):
     """Config 2: Llama-3-8B weight shapes, one GPU, end-to-end amax + 4/6 quantize."""
     import torch
 
-    import paper_2512_02010_b200 as f46
     from paper_2512_02010_b200 import _lib
+    from paper_2512_02010_b200.blockquant import scales_tc_bytes
 
-    shapes = [(4096, 4096), (4096, 14336), (14336, 4096)]
     stream = torch.cuda.current_stream()
     flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     out = {}
-    for (r, c) in shapes:
+    for (r, c) in [(4096, 4096), (4096, 14336), (14336, 4096)]:
         g = torch.Generator(device=dev).manual_seed(r * 7 + c)
         w = (torch.randn(r, c, generator=g, device=dev) * 0.02).to(torch.bfloat16)
         codes = torch.empty((r, c // 2), dtype=torch.uint8, device=dev)
-        scales = torch.empty(f46.blockquant.scales_tc_bytes(r, c), dtype=torch.uint8, device=dev)
+        scales = torch.empty(scales_tc_bytes(r, c), dtype=torch.uint8, device=dev)
         amax = torch.zeros(1, dtype=torch.float64, device=dev)
 
         def once():
@@ -356,7 +362,7 @@ def bench_weights(args, L, dev, peaks):
         ts = []
         for i in range(max(5, args.steps)):
             flush_buf.fill_(i & 0xFF)
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s, e = _events(2)
             s.record(stream)
             once()
             e.record(stream)
@@ -364,8 +370,123 @@ def bench_weights(args, L, dev, peaks):
             ts.append(s.elapsed_time(e))
         ms = sum(ts) / len(ts)
         gbs = w.numel() * BYTES_PER_ELEM / (ms * 1e-3) / 1e9
-        out[f"{r}x{c}"] = {"ms": ms, "GB/s": gbs, "frac_of_hbm": gbs / peaks["hbm_gbs"]}
+        out[f"{r}x{c}"] = {"ms": ms, "GB/s": gbs, "frac_of_hbm": gbs / peaks["hbm_gbs"],
+                           "note": "amax + fused 4/6 quantize, L2 flushed, N(0,0.02^2) bf16"}
     return out
+
+
+def bench_gemm(args, dev, peaks):
+    """Config 4: 8192^3 tcgen05 NVFP4 GEMM of two 4/6-quantized BF16 operands."""
+    import torch
+
+    import paper_2512_02010_b200 as f46
+
+    M = N = K = 8192
+    g = torch.Generator(device=dev).manual_seed(0)
+    cfg = f46.QuantConfig(scale_mode="adaptive")
+    xa = torch.randn(M, K, generator=g, device=dev).to(torch.bfloat16)
+    xb = torch.randn(N, K, generator=g, device=dev).to(torch.bfloat16)
+    aq = f46.quantize_tensor_adaptive(xa, cfg, check_finite=False)
+    bq = f46.quantize_tensor_adaptive(xb, cfg, check_finite=False)
+    out = {}
+    flops = 2.0 * M * N * K
+    stream = torch.cuda.current_stream()
+    for od, name in ((torch.bfloat16, "bf16"), (torch.float32, "f32")):
+        c = torch.empty((M, N), dtype=od, device=dev)
+        for _ in range(3):
+            f46.gemm_nvfp4(aq, bq, od, out=c)
+        reps = max(5, args.steps)
+        s, e = _events(2)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(reps):  # back to back: host launch work overlaps the GPU
+            f46.gemm_nvfp4(aq, bq, od, out=c)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        out[name] = {"ms": ms, "TFLOP/s": flops / (ms * 1e-3) / 1e12}
+    tf = out["bf16"]["TFLOP/s"]
+    fp4_from_bf16 = 4.0 * peaks["bf16_tflops"]
+
+    # quantize(A) + quantize(B) + GEMM through the public API, inputs resident
+    def full():
+        qa = f46.quantize_tensor_adaptive(xa, cfg, check_finite=False)
+        qb = f46.quantize_tensor_adaptive(xb, cfg, check_finite=False)
+        return f46.gemm_nvfp4(qa, qb, torch.bfloat16)
+
+    for _ in range(2):
+        full()
+    s, e = _events(2)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(5):
+        full()
+    e.record(stream)
+    torch.cuda.synchronize()
+    full_ms = s.elapsed_time(e) / 5
+    return {
+        "metric": "4/6-NVFP4 GEMM TFLOP/s", "shape": [M, N, K], "value": tf, "unit": "TFLOP/s",
+        "out": out,
+        "roofline": {"bound": "tensor", "kernel": "gemm_nvfp4_persistent<bf16>",
+                     "achieved": tf, "peak": FP4_DENSE_NOMINAL_TFLOPS,
+                     "peak_kind": "nominal dense FP4 (no measured FP4 peak on this pool)",
+                     "unit": "TFLOP/s", "frac": tf / FP4_DENSE_NOMINAL_TFLOPS,
+                     "frac_vs_4x_measured_bf16": tf / fp4_from_bf16,
+                     "algorithmic_flops_per_launch": flops, "launch_ms": out["bf16"]["ms"],
+                     "traffic": profile_traffic("gemm_nvfp4_persistent")},
+        "quantize_a_b_plus_gemm_ms": full_ms,
+        "data": "synthetic N(0,1) bf16 operands, both quantized with 4/6 (adaptive)",
+    }
+
+
+def bench_moe(args, dev):
+    """Config 5 (per GPU of an 8-GPU EP job): Nemotron-3-Nano experts, hidden
+    2688, FFN 1856, 3072 tokens per expert, 16 experts per GPU.  FPROP (x W1^T,
+    h W2^T) and WGRAD (dh^T x, dy^T h; contraction over tokens) as grouped
+    NVFP4 GEMMs of 4/6-quantized operands.  DGRAD needs W^T blocked along the
+    output dim (2-D tile quantization, a later row) and is not timed."""
+    import torch
+
+    import paper_2512_02010_b200 as f46
+
+    E, T, H, F = 16, 3072, 2688, 1856
+    cfg = f46.QuantConfig(scale_mode="adaptive")
+    g = torch.Generator(device=dev).manual_seed(5)
+
+    def qstack(rows, cols, std):
+        qs = [f46.quantize_tensor_adaptive(
+            (torch.randn(rows, cols, generator=g, device=dev) * std).to(torch.bfloat16), cfg,
+            check_finite=False) for _ in range(E)]
+        return (torch.stack([q.packed_codes for q in qs]), torch.stack([q.scales_tc for q in qs]),
+                torch.cat([q.alpha_dev for q in qs]))
+
+    gemms = {
+        "fprop_x_w1": (qstack(T, H, 1.0), qstack(F, H, 0.02), T, F, H),
+        "fprop_h_w2": (qstack(T, F, 1.0), qstack(H, F, 0.02), T, H, F),
+        "wgrad_dh_x": (qstack(F, T, 1e-3), qstack(H, T, 1.0), F, H, T),
+        "wgrad_dy_h": (qstack(H, T, 1e-3), qstack(F, T, 1.0), H, F, T),
+    }
+    stream = torch.cuda.current_stream()
+    res, tot_flops, tot_ms = {}, 0.0, 0.0
+    for name, (a, b, M, N, K) in gemms.items():
+        run = lambda: f46.gemm_nvfp4_grouped(a[0], a[1], a[2], b[0], b[1], b[2], M, N, K,
+                                             torch.bfloat16)
+        for _ in range(3):
+            run()
+        s, e = _events(2)
+        torch.cuda.synchronize()
+        s.record(stream)
+        for _ in range(5):
+            run()
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / 5
+        fl = 2.0 * E * M * N * K
+        res[name] = {"M": M, "N": N, "K": K, "experts": E, "ms": ms, "TFLOP/s": fl / (ms * 1e-3) / 1e12}
+        tot_flops += fl
+        tot_ms += ms
+    return {"per_gemm": res, "TFLOP/s": tot_flops / (tot_ms * 1e-3) / 1e12, "ms": tot_ms,
+            "note": "per GPU of EP=8: 8 GPUs x 8192 tokens x top-6 / 128 experts = 3072 tokens/expert"}
 
 
 def cpu_baseline(args):
@@ -387,18 +508,8 @@ def cpu_baseline(args):
     sec = time.perf_counter() - t0
     return {"value": bits.size * BYTES_PER_ELEM / sec / 1e9, "unit": "GB/s", "cores": cores,
             "kind": "port",
-            "sample": f"{rows}x{COLS} BF16 rows of the c3 tensor, oracle port (float64 restatement "
+            "sample": f"{rows}x{COLS} BF16 rows of the c3 tensor, oracle port (float64 C restatement "
                       f"of the reference), {cores} threads, {sec:.2f} s"}
-
-
-def bench_gemm(args, dev, peaks):
-    try:
-        import paper_2512_02010_b200 as f46
-        if not hasattr(f46, "gemm_nvfp4"):
-            return None
-        return f46.qlinear.bench_gemm(dev, peaks, steps=max(5, args.steps))
-    except Exception as e:  # the quantize headline stands without it
-        return {"error": repr(e)[:300]}
 
 
 def main():
@@ -407,7 +518,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--ref-rows", type=int, default=4096)
+    ap.add_argument("--ref-rows", type=int, default=8192)
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

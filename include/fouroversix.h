@@ -133,8 +133,11 @@ int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout
  * Block-scaled NVFP4 GEMM on tcgen05 (kind::mxf4nvf4, E4M3 scales, 16-blocks):
  *   C[M,N] = alpha_a * alpha_b * sum_k A[m,k] * B[n,k]
  * A and B are both K-major f46_quantize outputs ("TN": qlinear.py:74-93 with
- * transpose_b=True).  K must be a multiple of 64 (pad with zero blocks);
- * M, N arbitrary.  C is row-major [M][ldc] of c_dtype (F46_DT_F32 or F46_DT_BF16).
+ * transpose_b=True): codes [rows][ceil(K/16)*8] bytes, scales in the tcgen05
+ * layout, alpha as a device double.  ceil(K/16) must be even (16-byte code
+ * rows for TMA); M, N arbitrary.  C is row-major [M][ldc] of c_dtype
+ * (F46_DT_F32 or F46_DT_BF16), ldc >= N.  F46_ERR_UNSUPPORTED for odd
+ * ceil(K/16) or unaligned operand buffers.
  */
 int f46_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_scales_tc, const double* d_alpha_a,
                    const uint8_t* b_codes, const uint8_t* b_scales_tc, const double* d_alpha_b,
@@ -142,7 +145,9 @@ int f46_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_scales_tc, const dou
                    f46_stream_t stream);
 
 /* Grouped (MoE-style) variant: `groups` independent GEMMs of one shape whose
- * operands are packed back to back (stride = one operand's buffer size). */
+ * operands are packed back to back (group stride = one operand's code / scale
+ * buffer size), one alpha per group (d_alpha_a[g], d_alpha_b[g]); C is
+ * [groups][M][ldc]. */
 int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
                            const double* d_alpha_a, const uint8_t* b_codes,
                            const uint8_t* b_scales_tc, const double* d_alpha_b, int64_t M,
