@@ -455,6 +455,209 @@ __global__ void __launch_bounds__(kThreadsP, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256 x 256 tile.  Each CTA stages only its own 128 rows of A and
+// its own 128 rows of B (the two halves of N) plus the scale atoms, so a CTA
+// moves 38 KB per 256-wide K step instead of 54 KB; the leader CTA issues
+// one 256x256x64 MMA per K=64 that reads both CTAs' shared memory and writes
+// both CTAs' TMEM (each its 128 accumulator rows x 256 columns).  All loads
+// of both CTAs complete on the leader's `full` barrier; the leader's commits
+// multicast to both CTAs' `empty` / `acc_full` barriers; both CTAs'
+// epilogue warps arrive on the leader's `acc_empty`.
+// ---------------------------------------------------------------------------
+constexpr int kStagesPair = 5;
+constexpr int PA_BYTES = 128 * BK / 2;   // this CTA's 128 rows of A
+constexpr int PB_BYTES = 128 * BK / 2;   // this CTA's 128 rows of B
+constexpr int PSFA_BYTES = 2048;         // 4 atoms of this CTA's 128 A rows
+constexpr int PSFB_BYTES = 4096;         // 2 row tiles x 4 atoms: all 256 rows of the B tile
+constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES + PSFA_BYTES + PSFB_BYTES;
+constexpr int SMEM_BYTES_PAIR = kStagesPair * PSTAGE_BYTES + 1024 + 1024;
+constexpr uint32_t kIdescPair = (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                                ((uint32_t)(256 >> 4) << 24);
+
+template <int OUT_BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
+    gemm_nvfp4_pair(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_b,
+                    const __grid_constant__ CUtensorMap tmap_sfa,
+                    const __grid_constant__ CUtensorMap tmap_sfb, const GemmParams p, int groups) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~(uintptr_t)1023);
+  uint8_t* sm_a = smem;
+  uint8_t* sm_b = sm_a + kStagesPair * PA_BYTES;
+  uint8_t* sm_sfa = sm_b + kStagesPair * PB_BYTES;
+  uint8_t* sm_sfb = sm_sfa + kStagesPair * PSFA_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm_sfb + kStagesPair * PSFB_BYTES);
+  uint64_t* empty = full + kStagesPair;
+  uint64_t* acc_full = empty + kStagesPair;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int64_t nb = (p.K + 15) >> 4;
+  const int64_t kb4 = (nb + 3) >> 2;
+  const int ktiles = (int)((kb4 + 3) >> 2);
+  const int num_m = (int)((p.M + 255) / 256), num_n = (int)((p.N + BN - 1) / BN);
+  const int num_tiles = groups * num_m * num_n;
+  const int cid = (int)cluster_id_x(), ncl = (int)num_clusters_x();
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+    prefetch_tmap(&tmap_sfa);
+    prefetch_tmap(&tmap_sfb);
+    for (int s = 0; s < kStagesPair; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 2 * kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_holder, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers exist before anyone signals remotely
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (elect_one()) {
+      int it = 0;
+      for (int t = cid; t < num_tiles; t += ncl) {
+        const TileCoord tc = tile_of(t, num_m, num_n);
+        const int m0 = tc.mt * 256 + 128 * (int)rank;  // this CTA's A rows
+        const int n0 = tc.nt * BN;
+        const int nb0 = n0 + 128 * (int)rank;         // this CTA's B rows
+        // scale-atom rows of the 2-D (256-byte row) view of the scale buffers
+        const int sfa_row = (int)(2 * (int64_t)(m0 >> 7) * kb4);
+        const int sfb_row0 = (int)(2 * (int64_t)(n0 >> 7) * kb4);
+        const int sfb_row1 = (int)(2 * (int64_t)((n0 >> 7) + 1) * kb4);
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStagesPair;
+          if (it >= kStagesPair) mbar_wait(&empty[s], ((it / kStagesPair) - 1) & 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * PSTAGE_BYTES);
+          const uint32_t bar = smem_u32(&full[s]);
+          tma_load_3d_pair(smem_u32(sm_a + s * PA_BYTES), &tmap_a, bar, kt * (BK / 2), m0, tc.g);
+          tma_load_3d_pair(smem_u32(sm_b + s * PB_BYTES), &tmap_b, bar, kt * (BK / 2), nb0, tc.g);
+          tma_load_3d_pair(smem_u32(sm_sfa + s * PSFA_BYTES), &tmap_sfa, bar, 0, sfa_row + 8 * kt,
+                           tc.g);
+          tma_load_3d_pair(smem_u32(sm_sfb + s * PSFB_BYTES), &tmap_sfb, bar, 0,
+                           sfb_row0 + 8 * kt, tc.g);
+          tma_load_3d_pair(smem_u32(sm_sfb + s * PSFB_BYTES + 2048), &tmap_sfb, bar, 0,
+                           sfb_row1 + 8 * kt, tc.g);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader only)
+    if (leader && elect_one()) {
+      int it = 0, lt = 0;
+      for (int t = cid; t < num_tiles; t += ncl, ++lt) {
+        if (lt > 0) {
+          mbar_wait(acc_empty, (lt - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+          const int s = it % kStagesPair;
+          mbar_wait(&full[s], (it / kStagesPair) & 1);
+          tc_fence_after();
+          const int nk = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
+          const uint32_t tsfa = tmem + TM_SF + (it & 1) * TM_SF_BUF;
+          const uint32_t tsfb = tsfa + 16;
+          const uint32_t a_addr = smem_u32(sm_a + s * PA_BYTES);
+          const uint32_t b_addr = smem_u32(sm_b + s * PB_BYTES);
+          const uint32_t sfa_addr = smem_u32(sm_sfa + s * PSFA_BYTES);
+          const uint32_t sfb_addr = smem_u32(sm_sfb + s * PSFB_BYTES);
+          for (int j = 0; j < nk; ++j) {
+            tc_cp_32x128b_x4_pair(tsfa + 4 * j, smem_desc(sfa_addr + 512 * j, 0, 128, 0));
+            tc_cp_32x128b_x4_pair(tsfb + 8 * j, smem_desc(sfb_addr + 512 * j, 0, 128, 0));
+            tc_cp_32x128b_x4_pair(tsfb + 8 * j + 4, smem_desc(sfb_addr + 2048 + 512 * j, 0, 128, 0));
+          }
+          for (int j = 0; j < nk; ++j) {
+            const uint64_t ad = smem_desc(a_addr + 32 * j, 16, 1024, 2);
+            const uint64_t bd = smem_desc(b_addr + 32 * j, 16, 1024, 2);
+            mma_nvf4_pair(tmem, ad, bd, kIdescPair, (kt | j) != 0, tsfa + 4 * j, tsfb + 8 * j);
+          }
+          tc_commit_pair(&empty[s], 0x3);
+        }
+        tc_commit_pair(acc_full, 0x3);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const int h = (warp - 2) >> 2;
+    const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + 128 * h;
+    const uint32_t leader_acc_empty = mapa(smem_u32(acc_empty), 0);
+    int lt = 0;
+    for (int t = cid; t < num_tiles; t += ncl, ++lt) {
+      const TileCoord tc = tile_of(t, num_m, num_n);
+      const float alpha = (float)(p.alpha_a[tc.g * p.alpha_group_stride] *
+                                  p.alpha_b[tc.g * p.alpha_group_stride]);
+      mbar_wait(acc_full, lt & 1);
+      tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) tc_ld_32x32b_x32(taddr + 32 * i, r[i]);
+      tc_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+      const int64_t row = (int64_t)tc.mt * 256 + 128 * rank + 32 * q + lane;
+      if (row >= p.M) continue;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t col0 = (int64_t)tc.nt * BN + 128 * h + 32 * i;
+        if (col0 >= p.N) break;
+        if (OUT_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + tc.g * p.c_group_stride +
+                               row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint32_t w[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[i][j + 2 * k]) * alpha,
+                                                         __uint_as_float(r[i][j + 2 * k + 1]) * alpha);
+                w[k] = *reinterpret_cast<uint32_t*>(&v);
+              }
+              *reinterpret_cast<uint4*>(out + j) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+              out[j] = __float2bfloat16_rn(__uint_as_float(r[i][j]) * alpha);
+          }
+        } else {
+          float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + col0;
+          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(out + j) = make_float4(
+                  __uint_as_float(r[i][j]) * alpha, __uint_as_float(r[i][j + 1]) * alpha,
+                  __uint_as_float(r[i][j + 2]) * alpha, __uint_as_float(r[i][j + 3]) * alpha);
+          } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = __uint_as_float(r[i][j]) * alpha;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -490,6 +693,21 @@ bool make_code_map(CUtensorMap* m, const uint8_t* codes, int64_t groups, int64_t
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over the tcgen05-layout scale buffer viewed as [groups][bytes/256][256]
+// (uint8), box 256 x 8 rows = four 512-byte atoms, no swizzle; rows past the
+// buffer read as zero (a B tile's absent second row tile).
+bool make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t groups, int64_t group_bytes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {256, (cuuint64_t)(group_bytes / 256), (cuuint64_t)groups};
+  const cuuint64_t strides[2] = {256, (cuuint64_t)group_bytes};
+  const cuuint32_t box[3] = {256, 8, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(sf), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const double* alpha_a,
                 const uint8_t* b_codes, const uint8_t* b_sf, const double* alpha_b, int64_t M,
                 int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype, int alpha_per_group,
@@ -522,6 +740,42 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   p.c_group_stride = M * ldc;
   p.alpha_group_stride = alpha_per_group ? 1 : 0;
   p.c_bf16 = c_dtype == F46_DT_BF16;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  // CTA-pair (cta_group::2) kernel by default; F46_GEMM_1SM / F46_GEMM_SIMPLE
+  // select the single-CTA persistent / one-tile-per-CTA kernels.
+  const char* sel = getenv("F46_GEMM_KERNEL");
+  const bool want_pair = !getenv("F46_GEMM_SIMPLE") && !getenv("F46_GEMM_1SM") &&
+                         !(sel && sel[0] != 'p');
+  CUtensorMap msfa, msfb, mb_half;
+  if (want_pair && make_sf_map(&msfa, a_sf, groups, p.sfa_group_stride) &&
+      make_sf_map(&msfb, b_sf, groups, p.sfb_group_stride) &&
+      make_code_map(&mb_half, b_codes, groups, N, kbytes, 128)) {
+    static std::once_flag pair_once;
+    std::call_once(pair_once, [] {
+      cudaFuncSetAttribute(gemm_nvfp4_pair<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES_PAIR);
+      cudaFuncSetAttribute(gemm_nvfp4_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_BYTES_PAIR);
+    });
+    const int64_t tiles = (int64_t)groups * ((M + 255) / 256) * ((N + BN - 1) / BN);
+    const unsigned grid = 2u * (unsigned)std::min<int64_t>(tiles, sms / 2);
+    if (p.c_bf16)
+      gemm_nvfp4_pair<1><<<grid, kThreadsP, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+    else
+      gemm_nvfp4_pair<0><<<grid, kThreadsP, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      fprintf(stderr, "[fouroversix] gemm (pair) launch: %s\n", cudaGetErrorString(e));
+      return F46_ERR_CUDA;
+    }
+    return F46_OK;
+  }
   // Persistent kernel unless F46_GEMM_SIMPLE asks for the one-tile-per-CTA one.
   if (!getenv("F46_GEMM_SIMPLE")) {
     static std::once_flag pattr_once;
@@ -531,13 +785,6 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
       cudaFuncSetAttribute(gemm_nvfp4_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            SMEM_BYTES_P);
     });
-    static int sms = 0;
-    if (sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (sms <= 0) sms = 148;
-    }
     const int64_t tiles = (int64_t)groups * ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
     if (p.c_bf16)

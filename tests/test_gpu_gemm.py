@@ -147,16 +147,21 @@ def test_grouped_matches_per_group():
 
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
 def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
-    """The persistent kernel and the one-tile-per-CTA kernel (F46_GEMM_SIMPLE)
-    accumulate every tile in the same order: identical bits, also into a
-    strided output (ldc = N + 1)."""
+    """The CTA-pair kernel (default), the single-CTA persistent kernel
+    (F46_GEMM_1SM) and the one-tile-per-CTA kernel (F46_GEMM_SIMPLE) accumulate
+    every output element over K in the same order: identical bits, also into
+    a strided output (ldc = N + 1)."""
     M, N, K = 700, 1000, 1024
     aq = f46.quantize_tensor_adaptive(bf16_randn((M, K), 71).cuda(), ADAPT)
     bq = f46.quantize_tensor_adaptive(bf16_randn((N, K), 72).cuda(), ADAPT)
     fast = f46.gemm_nvfp4(aq, bq, out_dtype)
     wide = torch.empty((M, N + 1), dtype=out_dtype, device="cuda")
     strided = f46.gemm_nvfp4(aq, bq, out_dtype, out=wide[:, :N])
+    monkeypatch.setenv("F46_GEMM_1SM", "1")
+    one_sm = f46.gemm_nvfp4(aq, bq, out_dtype)
     monkeypatch.setenv("F46_GEMM_SIMPLE", "1")
     simple = f46.gemm_nvfp4(aq, bq, out_dtype)
-    assert torch.equal(fast, simple) and torch.equal(fast, strided)
+    assert torch.equal(one_sm, simple)
+    assert torch.equal(fast, strided)
+    assert torch.equal(fast, simple), "CTA-pair and single-CTA kernels differ"
     assert rel_fro(fast.float(), gpu_oracle(aq, bq)) <= (REL_TOL if out_dtype == torch.float32 else 4e-3)
