@@ -460,10 +460,19 @@ __global__ void __launch_bounds__(kThreadsP, 1)
 // its own 128 rows of B (the two halves of N) plus the scale atoms, so a CTA
 // moves 38 KB per 256-wide K step instead of 54 KB; the leader CTA issues
 // one 256x256x64 MMA per K=64 that reads both CTAs' shared memory and writes
-// both CTAs' TMEM (each its 128 accumulator rows x 256 columns).  All loads
-// of both CTAs complete on the leader's `full` barrier; the leader's commits
-// multicast to both CTAs' `empty` / `acc_full` barriers; both CTAs'
-// epilogue warps arrive on the leader's `acc_empty`.
+// both CTAs' TMEM (each its 128 accumulator rows x 256 columns).  A/B loads of
+// both CTAs complete on the leader's `full` barrier; the leader's commits
+// multicast to both CTAs' `empty` / `sf_empty` / `acc_full` barriers; both
+// CTAs' epilogue warps arrive on the leader's `acc_empty`.
+//
+// Scale factors reach TMEM through registers (tcgen05.st) written by four
+// dedicated warps per CTA, not tcgen05.cp.  The MMA's output rows 32q..32q+31
+// read their scales from TMEM lane quadrant q only (tools/sf_probe.cu): SFA
+// row m from column (m/32) of lane m, and every SFB row from that quadrant's
+// copy.  So SFA needs one column per quadrant and SFB one copy per quadrant --
+// 18 KB of TMEM writes per K step at the store path's rate, instead of 24 KB
+// through the slower, MMA-serialised copy path (tools/mma_rate.cu: 12 copies
+// per 4 MMAs cost 86 extra cycles per MMA).
 // ---------------------------------------------------------------------------
 constexpr int kStagesPair = 5;
 constexpr int PA_BYTES = 128 * BK / 2;   // this CTA's 128 rows of A
@@ -472,11 +481,14 @@ constexpr int PSFA_BYTES = 2048;         // 4 atoms of this CTA's 128 A rows
 constexpr int PSFB_BYTES = 4096;         // 2 row tiles x 4 atoms: all 256 rows of the B tile
 constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES + PSFA_BYTES + PSFB_BYTES;
 constexpr int SMEM_BYTES_PAIR = kStagesPair * PSTAGE_BYTES + 1024 + 1024;
+constexpr int kSfWarps = 4;
+constexpr int kSfBufs = 4;  // TMEM scale buffers: 256 + 4 x 48 = 448 columns
+constexpr int kThreadsPair = 64 + 32 * kEpiWarps + 32 * kSfWarps;
 constexpr uint32_t kIdescPair = (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                 ((uint32_t)(256 >> 4) << 24);
 
 template <int OUT_BF16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_nvfp4_pair(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_sfa,
@@ -490,7 +502,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
   uint8_t* sm_sfb = sm_sfa + kStagesPair * PSFA_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm_sfb + kStagesPair * PSFB_BYTES);
   uint64_t* empty = full + kStagesPair;
-  uint64_t* acc_full = empty + kStagesPair;
+  uint64_t* sf_ld_full = empty + kStagesPair;  // this CTA's scale atoms landed in smem
+  uint64_t* sf_full = sf_ld_full + kStagesPair;  // scales in TMEM (leader: 8 warps of 2 CTAs)
+  uint64_t* acc_full = sf_full + kSfBufs;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
@@ -512,6 +526,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
     for (int s = 0; s < kStagesPair; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&sf_ld_full[s], 1);
+    }
+    for (int b = 0; b < kSfBufs; ++b) {
+      mbar_init(&sf_full[b], 2 * kSfWarps);
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 2 * kEpiWarps);
@@ -540,16 +558,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStagesPair;
           if (it >= kStagesPair) mbar_wait(&empty[s], ((it / kStagesPair) - 1) & 1);
-          if (leader) mbar_expect_tx(&full[s], 2 * PSTAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[s], 2 * (PA_BYTES + PB_BYTES));
           const uint32_t bar = smem_u32(&full[s]);
           tma_load_3d_pair(smem_u32(sm_a + s * PA_BYTES), &tmap_a, bar, kt * (BK / 2), m0, tc.g);
           tma_load_3d_pair(smem_u32(sm_b + s * PB_BYTES), &tmap_b, bar, kt * (BK / 2), nb0, tc.g);
-          tma_load_3d_pair(smem_u32(sm_sfa + s * PSFA_BYTES), &tmap_sfa, bar, 0, sfa_row + 8 * kt,
-                           tc.g);
-          tma_load_3d_pair(smem_u32(sm_sfb + s * PSFB_BYTES), &tmap_sfb, bar, 0,
-                           sfb_row0 + 8 * kt, tc.g);
-          tma_load_3d_pair(smem_u32(sm_sfb + s * PSFB_BYTES + 2048), &tmap_sfb, bar, 0,
-                           sfb_row1 + 8 * kt, tc.g);
+          mbar_expect_tx(&sf_ld_full[s], PSFA_BYTES + PSFB_BYTES);
+          tma_load_3d(smem_u32(sm_sfa + s * PSFA_BYTES), &tmap_sfa, &sf_ld_full[s], 0,
+                      sfa_row + 8 * kt, tc.g);
+          tma_load_3d(smem_u32(sm_sfb + s * PSFB_BYTES), &tmap_sfb, &sf_ld_full[s], 0,
+                      sfb_row0 + 8 * kt, tc.g);
+          tma_load_3d(smem_u32(sm_sfb + s * PSFB_BYTES + 2048), &tmap_sfb, &sf_ld_full[s], 0,
+                      sfb_row1 + 8 * kt, tc.g);
         }
       }
     }
@@ -564,20 +583,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
         }
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStagesPair;
+          const int b = it % kSfBufs;
           mbar_wait(&full[s], (it / kStagesPair) & 1);
+#if F46_GEMM_DEBUG != 7
+          mbar_wait(&sf_full[b], (it / kSfBufs) & 1);
+#endif
           tc_fence_after();
           const int nk = (int)min((int64_t)4, kb4 - 4 * (int64_t)kt);
-          const uint32_t tsfa = tmem + TM_SF + (it & 1) * TM_SF_BUF;
+          const uint32_t tsfa = tmem + TM_SF + b * TM_SF_BUF;
           const uint32_t tsfb = tsfa + 16;
           const uint32_t a_addr = smem_u32(sm_a + s * PA_BYTES);
           const uint32_t b_addr = smem_u32(sm_b + s * PB_BYTES);
-          const uint32_t sfa_addr = smem_u32(sm_sfa + s * PSFA_BYTES);
-          const uint32_t sfb_addr = smem_u32(sm_sfb + s * PSFB_BYTES);
-          for (int j = 0; j < nk; ++j) {
-            tc_cp_32x128b_x4_pair(tsfa + 4 * j, smem_desc(sfa_addr + 512 * j, 0, 128, 0));
-            tc_cp_32x128b_x4_pair(tsfb + 8 * j, smem_desc(sfb_addr + 512 * j, 0, 128, 0));
-            tc_cp_32x128b_x4_pair(tsfb + 8 * j + 4, smem_desc(sfb_addr + 2048 + 512 * j, 0, 128, 0));
-          }
           for (int j = 0; j < nk; ++j) {
             const uint64_t ad = smem_desc(a_addr + 32 * j, 16, 1024, 2);
             const uint64_t bd = smem_desc(b_addr + 32 * j, 16, 1024, 2);
@@ -586,6 +602,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
           tc_commit_pair(&empty[s], 0x3);
         }
         tc_commit_pair(acc_full, 0x3);
+      }
+    }
+  } else if (warp >= 2 + kEpiWarps) {
+    // ------------------------------------------------------------ scale-factor writers
+    const int q = warp & 3;  // TMEM lane quadrant = output row block this warp feeds
+    const uint32_t lane_taddr = tmem + ((uint32_t)(32 * q) << 16);
+    const uint32_t leader_sf_full = mapa(smem_u32(&sf_full[0]), 0);
+    int it = 0;
+    for (int t = cid; t < num_tiles; t += ncl) {
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = it % kStagesPair;
+        const int b = it % kSfBufs;
+        mbar_wait(&sf_ld_full[s], (it / kStagesPair) & 1);
+        // buffer b was last read by the MMAs of iteration it - kSfBufs, whose
+        // completion the (multicast) commit on that iteration's `empty` signals
+        if (it >= kSfBufs) {
+          const int prev = it - kSfBufs;
+          mbar_wait(&empty[prev % kStagesPair], (prev / kStagesPair) & 1);
+        }
+        tc_fence_after();
+#if F46_GEMM_DEBUG == 6
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_sf_full + 8 * b);
+        continue;
+#endif
+        // SFA: row 32q+lane, k-group j = word q of atom j, row `lane`
+        const uint8_t* sa = sm_sfa + s * PSFA_BYTES + lane * 16 + q * 4;
+        uint32_t va[16];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(sa + 512 * j);
+          va[4 * j] = va[4 * j + 1] = va[4 * j + 2] = va[4 * j + 3] = w;
+        }
+        // SFB: column 8j + 4t + w = B row 32(4t+w) + lane, k-group j
+        const uint8_t* sb = sm_sfb + s * PSFB_BYTES + lane * 16;
+        uint32_t vb[32];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+          for (int t2 = 0; t2 < 2; ++t2) {
+            const uint4 w = *reinterpret_cast<const uint4*>(sb + 2048 * t2 + 512 * j);
+            vb[8 * j + 4 * t2] = w.x;
+            vb[8 * j + 4 * t2 + 1] = w.y;
+            vb[8 * j + 4 * t2 + 2] = w.z;
+            vb[8 * j + 4 * t2 + 3] = w.w;
+          }
+        }
+        const uint32_t tsfa = lane_taddr + TM_SF + b * TM_SF_BUF;
+        tc_st_32x32b_x16(tsfa, va);
+        tc_st_32x32b_x32(tsfa + 16, vb);
+        tc_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_sf_full + 8 * b);
       }
     }
   } else {
@@ -601,48 +671,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsP, 1)
                                   p.alpha_b[tc.g * p.alpha_group_stride]);
       mbar_wait(acc_full, lt & 1);
       tc_fence_after();
-      uint32_t r[4][32];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) tc_ld_32x32b_x32(taddr + 32 * i, r[i]);
-      tc_wait_ld();
-      tc_fence_before();
+#if F46_GEMM_DEBUG == 5
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+      continue;
+#endif
       const int64_t row = (int64_t)tc.mt * 256 + 128 * rank + 32 * q + lane;
-      if (row >= p.M) continue;
+      const int64_t colh = (int64_t)tc.nt * BN + 128 * h;
+      if (OUT_BF16) {
+        // each 32-column slice is converted and stored as soon as it is loaded
+        // (stores are fire-and-forget); TMEM is released after the last load
+        __nv_bfloat16* out =
+            reinterpret_cast<__nv_bfloat16*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + colh;
+        const bool vec = colh + 128 <= p.N && (((uintptr_t)out) & 15) == 0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t col0 = (int64_t)tc.nt * BN + 128 * h + 32 * i;
-        if (col0 >= p.N) break;
-        if (OUT_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + tc.g * p.c_group_stride +
-                               row * p.ldc + col0;
-          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint32_t w[4];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[i][j + 2 * k]) * alpha,
-                                                         __uint_as_float(r[i][j + 2 * k + 1]) * alpha);
-                w[k] = *reinterpret_cast<uint32_t*>(&v);
-              }
-              *reinterpret_cast<uint4*>(out + j) = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          } else {
-            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
-              out[j] = __float2bfloat16_rn(__uint_as_float(r[i][j]) * alpha);
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[32];
+          tc_ld_32x32b_x32(taddr + 32 * i, r);
+          tc_wait_ld();
+          if (i == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
           }
-        } else {
-          float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + col0;
-          if (col0 + 32 <= p.N && (((uintptr_t)out) & 15) == 0) {
+          if (row >= p.M) continue;
+          uint32_t w[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * k]) * alpha,
+                                                     __uint_as_float(r[2 * k + 1]) * alpha);
+            w[k] = *reinterpret_cast<uint32_t*>(&v);
+          }
+          if (vec) {
+#pragma unroll
+            for (int k = 0; k < 16; k += 4)
+              *reinterpret_cast<uint4*>(out + 32 * i + 2 * k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+          } else {
+            for (int e = 0; e < 32; ++e)
+              if (colh + 32 * i + e < p.N)
+                reinterpret_cast<uint16_t*>(out)[32 * i + e] = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
+          }
+        }
+      } else {
+        // f32: store each 32-column slice as soon as it is loaded, release after the last
+        float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + colh;
+        const bool vec = colh + 128 <= p.N && (((uintptr_t)out) & 15) == 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[32];
+          tc_ld_32x32b_x32(taddr + 32 * i, r);
+          tc_wait_ld();
+          if (i == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+          }
+          if (row >= p.M) continue;
+          if (vec) {
 #pragma unroll
             for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(out + j) = make_float4(
-                  __uint_as_float(r[i][j]) * alpha, __uint_as_float(r[i][j + 1]) * alpha,
-                  __uint_as_float(r[i][j + 2]) * alpha, __uint_as_float(r[i][j + 3]) * alpha);
+              *reinterpret_cast<float4*>(out + 32 * i + j) = make_float4(
+                  __uint_as_float(r[j]) * alpha, __uint_as_float(r[j + 1]) * alpha,
+                  __uint_as_float(r[j + 2]) * alpha, __uint_as_float(r[j + 3]) * alpha);
           } else {
-            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = __uint_as_float(r[i][j]) * alpha;
+            for (int j = 0; j < 32; ++j)
+              if (colh + 32 * i + j < p.N) out[32 * i + j] = __uint_as_float(r[j]) * alpha;
           }
         }
       }
@@ -766,9 +859,9 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
     const int64_t tiles = (int64_t)groups * ((M + 255) / 256) * ((N + BN - 1) / BN);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(tiles, sms / 2);
     if (p.c_bf16)
-      gemm_nvfp4_pair<1><<<grid, kThreadsP, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+      gemm_nvfp4_pair<1><<<grid, kThreadsPair, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
     else
-      gemm_nvfp4_pair<0><<<grid, kThreadsP, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+      gemm_nvfp4_pair<0><<<grid, kThreadsPair, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       fprintf(stderr, "[fouroversix] gemm (pair) launch: %s\n", cudaGetErrorString(e));
