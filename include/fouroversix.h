@@ -107,14 +107,21 @@ int f46_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int mode,
 
 /*
  * 2-D 16x16-tile quantization of a [R, C] weight (transforms.py:134-179):
- * one E4M3 scale per tile (written to every row of the tile in both scale
- * layouts), FP4 codes in the same packed layout.  W and W^T quantized this
- * way are transposes of each other.
+ * one E4M3 scale per tile chosen over all 256 values (written to every row of
+ * the tile), FP4 codes in the same packed layout as f46_quantize.  Because a
+ * tile's scale is shared, W^T quantized this way is the transpose: with
+ * codes_t / scales_tc_t non-null the kernel also writes W^T ([C, R], packed
+ * codes [C][ceil(R/16)*8], tcgen05-layout scales) -- the K-major operand of
+ * the DGRAD GEMM dx = dy @ W (qlinear.py:123-135).  scales_tc and
+ * scales_tc_t must be zero-initialised by the caller (pad entries are not
+ * written).  Exact float64 arithmetic, numpy's pairwise order for the tile
+ * error sums.
  */
 int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, int rule,
                     double mcap, const double* d_amax, double alpha_override, uint8_t* codes,
-                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, double* d_alpha_out,
-                    uint32_t* d_flags, f46_stream_t stream);
+                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, uint8_t* codes_t,
+                    uint8_t* scales_tc_t, double* d_alpha_out, uint32_t* d_flags,
+                    f46_stream_t stream);
 
 /*
  * Dequantize (blockquant.py:363-376): out = decode_fp4(code) * alpha * decode(scale).

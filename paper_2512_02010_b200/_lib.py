@@ -57,7 +57,7 @@ def _declare(L):
     q_args = [p, i, i64, i64, i, i, d, p, d, p, p, p, p, p, p, p]
     L.f46_quantize.argtypes = q_args
     L.f46_quantize.restype = i
-    L.f46_quantize_2d.argtypes = q_args
+    L.f46_quantize_2d.argtypes = [p, i, i64, i64, i, i, d, p, d, p, p, p, p, p, p, p, p, p]
     L.f46_quantize_2d.restype = i
     L.f46_dequantize.argtypes = [p, p, i, p, i64, i64, p, i, p, p]
     L.f46_dequantize.restype = i

@@ -932,9 +932,4 @@ int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_
                      N, K, c, ldc, c_dtype, 1, (cudaStream_t)stream);
 }
 
-int f46_quantize_2d(const void*, int, int64_t, int64_t, int, int, double, const double*, double,
-                    uint8_t*, uint8_t*, uint8_t*, uint8_t*, double*, uint32_t*, f46_stream_t) {
-  return F46_ERR_UNSUPPORTED;
-}
-
 }  // extern "C"

@@ -541,6 +541,185 @@ __global__ void __launch_bounds__(256) quant_generic_kernel(QParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// 2-D 16x16-tile quantization (transforms.py:108-179 _tile_pass /
+// quantize_weights_2d): one E4M3 scale per 16x16 tile chosen over all 256
+// values, so the same codes and scales quantize W along its rows and W^T
+// along its rows -- FPROP (x W^T) and DGRAD (dy W) both get a K-major operand
+// from one pass.  One warp per tile, lane l owns tile row l/2, columns
+// 8(l%2)..+7.  The arithmetic is the reference's float64 restatement
+// (exact_pass' operations), and the 256-term error sums follow numpy's
+// pairwise order for the (16,16) axis pair: P(e[0:128]) + P(e[128:256]),
+// P with 8 accumulators r_j = e_j + e_{j+8} + e_{j+16} + ... in sequence
+// (checked against the reference: tests/golden/golden_tile2d.npz).  Weights
+// are quantized once per update, so exactness is bought with f64 here.
+// ---------------------------------------------------------------------------
+struct Q2Params {
+  const void* w;
+  int64_t R, C;
+  int mode, rule, dtype;
+  double mcap;
+  const double* d_amax;
+  double alpha_override;
+  uint8_t* codes;      // [R][nbC*8]
+  uint8_t* scales_tc;  // tcgen05 layout of [R, C]
+  uint8_t* scales_rm;  // [R][nbC] (nullable)
+  uint8_t* pick4;      // [R][nbC] (nullable)
+  uint8_t* codes_t;    // W^T: [C][nbR*8] (nullable)
+  uint8_t* scales_tc_t;  // tcgen05 layout of [C, R] (nullable)
+  double* d_alpha_out;
+  uint32_t* d_flags;
+};
+
+__device__ __forceinline__ double q2_load(const Q2Params& p, int64_t r, int64_t c) {
+  if (r >= p.R || c >= p.C) return 0.0;
+  const int64_t i = r * p.C + c;
+  if (p.dtype == DT_BF16)
+    return (double)__uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(p.w)[i] << 16);
+  if (p.dtype == DT_F32) return (double)reinterpret_cast<const float*>(p.w)[i];
+  return reinterpret_cast<const double*>(p.w)[i];
+}
+
+// numpy pairwise sum of the 256 tile errors; e[] in shared memory, row-major tile order
+__device__ __forceinline__ double pw_tile(const double* e) {
+  double tot = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = e[128 * h + j];
+    for (int i = 8; i < 128; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], e[128 * h + i + j]);
+    const double part = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                  __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    tot = h == 0 ? part : __dadd_rn(tot, part);
+  }
+  return tot;
+}
+
+__global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
+  __shared__ double esq[8][256];
+  __shared__ double eab[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t TR = (p.R + 15) >> 4, TC = (p.C + 15) >> 4;
+  const int64_t ntiles = TR * TC;
+  double alpha = p.alpha_override;
+  if (!(alpha > 0.0)) {
+    const double amax = *p.d_amax;
+    alpha = amax == 0.0 ? 1.0 : (double)((float)amax / (float)p.mcap);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.d_alpha_out) *p.d_alpha_out = alpha;
+    if (p.alpha_override <= 0.0 && p.d_flags && !(*p.d_amax <= 1.7976931348623157e308))
+      atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+  }
+  const int64_t nbC = (p.C + 15) >> 4, nbR = (p.R + 15) >> 4;
+  const int64_t kb4 = (nbC + 3) >> 2, kb4t = (nbR + 3) >> 2;
+  const int tr_local = lane >> 1, tc_half = lane & 1;  // tile row, 8-column half
+  double* es = esq[warp];
+  double* ea = eab[warp];
+  for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
+    const int64_t tr = tile / TC, tc = tile - tr * TC;
+    const int64_t r = tr * 16 + tr_local, c0 = tc * 16 + 8 * tc_half;
+    double x[8];
+    double tmax = 0.0;
+    bool nf = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i] = q2_load(p, r, c0 + i);
+      nf |= !(fabs(x[i]) <= 1.7976931348623157e308);
+      tmax = fmax(tmax, fabs(x[i]));
+    }
+    if (nf && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xFFFFFFFFu, tmax, o));
+    uint32_t sc[2];
+    uint32_t cw[2];  // 8 nibbles per candidate
+    double err[2];
+    const int ncand = p.mode == ADAPTIVE ? 2 : 1;
+    for (int k = 0; k < ncand; ++k) {
+      const double m = (p.mode == FIXED4 || k == 1) ? 4.0 : 6.0;
+      uint32_t s = enc_e4m3_d(__ddiv_rn(tmax, __dmul_rn(alpha, m)));
+      if (tmax == 0.0) s = 1;
+      const double denom = __dmul_rn(alpha, dec_e4m3_d(s));
+      uint32_t w = 0;
+      double mx = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double q = denom > 0.0 ? __ddiv_rn(x[i], denom)
+                                     : ((x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0);
+        const uint32_t code = enc_fp4_d(q);
+        w |= code << (4 * i);
+        const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(code), denom), x[i]);
+        es[tr_local * 16 + 8 * tc_half + i] = __dmul_rn(diff, diff);
+        ea[tr_local * 16 + 8 * tc_half + i] = fabs(diff);
+        mx = fmax(mx, fabs(diff));
+      }
+      __syncwarp();
+      double e;
+      if (p.rule == RULE_ABSMAX) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        e = mx;
+      } else {
+        e = __shfl_sync(0xFFFFFFFFu, lane == 0 ? pw_tile(p.rule == RULE_MSE ? es : ea) : 0.0, 0);
+      }
+      __syncwarp();
+      sc[k] = s;
+      cw[k] = w;
+      err[k] = e;
+    }
+    const bool k4 = (p.mode == ADAPTIVE) ? (err[1] < err[0]) : (p.mode == FIXED4);
+    const int ki = (p.mode == ADAPTIVE && k4) ? 1 : 0;
+    uint32_t w = cw[ki];
+    const uint32_t s = sc[ki];
+    // zero the codes of pad columns (x = 0 there; only -0.0 could leak a sign)
+    if (c0 + 8 > p.C) {
+      const int valid = (int)max((int64_t)0, p.C - c0);
+      w &= valid >= 8 ? 0xFFFFFFFFu : ((1u << (4 * valid)) - 1u);
+    }
+    if (r < p.R) {
+      reinterpret_cast<uint32_t*>(p.codes + r * nbC * 8)[2 * tc + tc_half] = w;
+      if (tc_half == 0) {
+        p.scales_tc[sf_tc_offset(r, tc, kb4)] = (uint8_t)s;
+        if (p.scales_rm) p.scales_rm[r * nbC + tc] = (uint8_t)s;
+        if (p.pick4) p.pick4[r * nbC + tc] = (uint8_t)k4;
+      }
+    }
+    if (p.codes_t) {
+      // W^T: tile row tr_local / column c of the tile -> W^T row (tc*16 + col),
+      // nibble position tr_local inside W^T's block tr.  Lane l gathers the
+      // 16 codes of W^T row tc*16 + l/2 ... through the warp.
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc) {
+        // code of element (row tr_local, col cc): held by lane 2*tr_local + cc/8
+        const int src = 2 * (lane & 15) + (cc >> 3);
+        const uint32_t wv = __shfl_sync(0xFFFFFFFFu, w, src);
+        const uint32_t code = (wv >> (4 * (cc & 7))) & 0xFu;
+        // lanes 0..15 build W^T row (tc*16 + cc)'s nibble (lane) for lane < 16
+        const uint32_t part = code << (4 * ((lane & 15) & 7));
+        uint32_t acc = part;
+        // OR-reduce within groups of 8 lanes (lanes 0-7 -> low word, 8-15 -> high word)
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+        const int64_t rt = tc * 16 + cc;  // W^T row
+        if (lane < 16 && (lane & 7) == 0 && rt < p.C) {
+          const int64_t ct0 = tr * 16 + 8 * (lane >> 3);  // W^T columns of this word
+          uint32_t wt = acc;
+          if (ct0 + 8 > p.R) {
+            const int valid = (int)max((int64_t)0, p.R - ct0);
+            wt &= valid >= 8 ? 0xFFFFFFFFu : ((1u << (4 * valid)) - 1u);
+          }
+          reinterpret_cast<uint32_t*>(p.codes_t + rt * nbR * 8)[2 * tr + (lane >> 3)] = wt;
+        }
+      }
+      if (p.scales_tc_t && lane < 16 && tc * 16 + lane < p.C)
+        p.scales_tc_t[sf_tc_offset(tc * 16 + lane, tr, kb4t)] = (uint8_t)s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1: amax
 // ---------------------------------------------------------------------------
 template <int DT>
@@ -893,6 +1072,29 @@ int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout
       return F46_ERR_INVALID_ARG;
   }
 #undef F46_DQ
+  return launch_status();
+}
+
+int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, int rule,
+                    double mcap, const double* d_amax, double alpha_override, uint8_t* codes,
+                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, uint8_t* codes_t,
+                    uint8_t* scales_tc_t, double* d_alpha_out, uint32_t* d_flags,
+                    f46_stream_t stream) {
+  if (!w || !codes || !scales_tc || R <= 0 || C <= 0) return F46_ERR_INVALID_ARG;
+  if (mode < F46_FIXED6 || mode > F46_ADAPTIVE || rule < F46_RULE_MSE || rule > F46_RULE_ABSMAX)
+    return F46_ERR_CONFIG;
+  if (dtype != F46_DT_F32 && dtype != F46_DT_BF16 && dtype != F46_DT_F64) return F46_ERR_INVALID_ARG;
+  if (alpha_override <= 0.0 && (!d_amax || !(mcap > 0.0))) return F46_ERR_INVALID_ARG;
+  if ((codes_t == nullptr) != (scales_tc_t == nullptr)) return F46_ERR_INVALID_ARG;
+  Q2Params p{w, R, C, mode, rule, dtype, mcap, d_amax, alpha_override, codes, scales_tc,
+             scales_rm, pick4, codes_t, scales_tc_t, d_alpha_out, d_flags};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t tiles = ((R + 15) / 16) * ((C + 15) / 16);
+  int64_t grid = (tiles + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  quant2d_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
   return launch_status();
 }
 

@@ -25,9 +25,10 @@ import torch
 
 from . import _lib
 from .blockquant import QuantizedTensor, _stream, dequantize_tensor
-from .errors import InvalidInputError
+from .errors import ConfigError, InvalidInputError
 
-__all__ = ["emulated_fp4_matmul", "gemm_nvfp4", "gemm_nvfp4_grouped", "round_to_bf16"]
+__all__ = ["emulated_fp4_matmul", "gemm_nvfp4", "gemm_nvfp4_grouped", "linear_dgrad",
+           "linear_forward", "linear_wgrad", "round_to_bf16"]
 
 
 def round_to_bf16(x: torch.Tensor) -> torch.Tensor:
@@ -49,9 +50,16 @@ def gemm_nvfp4(aq: QuantizedTensor, bq: QuantizedTensor, out_dtype=torch.float32
     dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16}[out_dtype]
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype, device=dev)
-    rc = L.f46_gemm_nvfp4(aq.packed_codes.data_ptr(), aq.scales_tc.data_ptr(),
-                          aq.alpha_dev.data_ptr(), bq.packed_codes.data_ptr(),
-                          bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, K,
+    a_codes, b_codes, k_eff = aq.packed_codes, bq.packed_codes, K
+    if (-(-K // 16)) % 2:
+        # TMA needs 16-byte code rows: append one all-zero 16-element block
+        # (its scales are already zero in the tcgen05 layout's padding)
+        a_codes = torch.nn.functional.pad(a_codes, (0, 8))
+        b_codes = torch.nn.functional.pad(b_codes, (0, 8))
+        k_eff = (-(-K // 16) + 1) * 16
+    rc = L.f46_gemm_nvfp4(a_codes.data_ptr(), aq.scales_tc.data_ptr(),
+                          aq.alpha_dev.data_ptr(), b_codes.data_ptr(),
+                          bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, k_eff,
                           out.data_ptr(), out.stride(0), dt, _stream())
     _lib.check(rc, "f46_gemm_nvfp4")
     return out
@@ -96,3 +104,59 @@ def emulated_fp4_matmul(aq: QuantizedTensor, bq: QuantizedTensor, *, transpose_b
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
     return round_to_bf16(C) if bf16_out else C
+
+
+def _quantize_1d(X, config, sr_tag: int = 0):
+    """qlinear.py:96-99: 4/6 or fixed quantization along the last dim."""
+    from .adaptive import quantize_tensor_adaptive
+    from .blockquant import quantize_tensor
+
+    if config.scale_mode == "adaptive":
+        return quantize_tensor_adaptive(X, config, sr_tag=sr_tag)
+    return quantize_tensor(X, config, sr_tag=sr_tag)
+
+
+def _check_2d(name: str, t) -> None:
+    if len(tuple(t.shape)) != 2:
+        raise InvalidInputError(f"{name} must be 2-D")
+
+
+def linear_forward(x, W, config, *, bf16_out: bool = False) -> torch.Tensor:
+    """y = q(x) @ q(W)^T, both operands RNE (qlinear.py:107-120): x blocked 1-D
+    along `in`, W in 16x16 tiles; the GEMM runs on tcgen05."""
+    from dataclasses import replace
+
+    from .transforms import quantize_weights_2d
+
+    _check_2d("x", x)
+    _check_2d("W", W)
+    if x.shape[1] != W.shape[1]:
+        raise InvalidInputError("x and W disagree on the input dimension")
+    rne = replace(config, rounding="rne")
+    xq = _quantize_1d(x, rne, sr_tag=0)
+    wq = quantize_weights_2d(W, rne, with_transpose=False)
+    return emulated_fp4_matmul(xq, wq, transpose_b=True, bf16_out=bf16_out)
+
+
+def linear_dgrad(dy, W, config, *, bf16_out: bool = False) -> torch.Tensor:
+    """dx = q(dy) @ q(W) (qlinear.py:123-135).  dy is blocked along `out`; W's
+    16x16 tiles make W^T an NVFP4 tensor blocked along `out` too, so the
+    product is a K-major (TN) tcgen05 GEMM against the transposed container."""
+    from dataclasses import replace
+
+    from .transforms import quantize_weights_2d
+
+    _check_2d("dy", dy)
+    _check_2d("W", W)
+    if dy.shape[1] != W.shape[0]:
+        raise InvalidInputError("dy and W disagree on the output dimension")
+    dyq = _quantize_1d(dy, config, sr_tag=1)
+    wq = quantize_weights_2d(W, replace(config, rounding="rne"))
+    return emulated_fp4_matmul(dyq, wq.transposed, transpose_b=True, bf16_out=bf16_out)
+
+
+def linear_wgrad(dy, x, config, *, bf16_out: bool = False):
+    """dW = q(T dy)^T @ q(T x) (qlinear.py:138-159) needs the randomized
+    Hadamard transform along the batch, which is not on the B200 path yet."""
+    raise ConfigError("linear_wgrad needs the randomized Hadamard transform (SURVEY.md 8(f) "
+                      "row 2), not implemented on the B200 path yet")

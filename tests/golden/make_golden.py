@@ -235,5 +235,30 @@ def main():
     print(f"wrote {len(gnames)} gemm cases to {path}")
 
 
+def linear_cases():
+    """Reference linear_forward / linear_dgrad (qlinear.py:107-135) on bf16-exact inputs."""
+    out, names = {}, []
+    for i, (B, IN, OUT, mode) in enumerate([(32, 64, 48, "adaptive"), (48, 96, 80, "fixed6"),
+                                             (40, 160, 64, "adaptive")]):
+        x = bf16(philox(900 + i).standard_normal((B, IN)))
+        W = bf16(philox(950 + i).standard_normal((OUT, IN)) * 0.05)
+        dy = bf16(philox(980 + i).standard_normal((B, OUT)))
+        cfg = fp4emu.QuantConfig(scale_mode=mode)
+        y = fp4emu.linear_forward(bf16_to_f64(x), bf16_to_f64(W), cfg)
+        dx = fp4emu.linear_dgrad(bf16_to_f64(dy), bf16_to_f64(W), cfg)
+        name = f"linear_{B}x{IN}x{OUT}_{mode}"
+        names.append(name)
+        for k, v in dict(x=x, W=W, dy=dy, y=y, dx=dx, mode=np.array(mode)).items():
+            out[f"{name}::{k}"] = v
+    out["__names__"] = np.array(names)
+    path = os.path.join(HERE, "golden_linear.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(names)} linear cases to {path}")
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "linear":
+        linear_cases()
+    else:
+        main()
+        linear_cases()

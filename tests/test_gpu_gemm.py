@@ -59,7 +59,7 @@ def oracle_product(x: torch.Tensor, w: torch.Tensor):
     return torch.from_numpy(dx @ dw.T)
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 256), (256, 512, 1024), (200, 300, 320),
+@pytest.mark.parametrize("M,N,K", [(128, 256, 256), (256, 512, 1024), (200, 300, 320), (64, 80, 48), (33, 70, 208),
                                    (1, 16, 64), (130, 260, 96), (384, 256, 4096)])
 def test_matches_oracle_small(M, N, K):
     x = bf16_randn((M, K), M + K)

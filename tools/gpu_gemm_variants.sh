@@ -1,1 +1,1 @@
-for so in build/variants/*.so; do echo $so; F46_LIB_PATH=$so timeout 120 python tools/time_gemm.py 8192 8192 8192 bf16; done
+for so in build/variants/*.so; do echo $so; F46_LIB_PATH=$so timeout 120 python tools/time_gemm.py 8192 8192 8192 bf16 2>&1 | tail -1; done
