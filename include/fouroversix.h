@@ -161,6 +161,18 @@ int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_
                            int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
                            f46_stream_t stream);
 
+/*
+ * Selection statistics of the 4/6 rules in one pass (adaptive.py:159-187):
+ * for every block both candidates' exact float64 errors and each rule's
+ * pick (mse / l1 / absmax, strict '<').  Writes d_partials[nparts][9] =
+ * {4-picks mse, l1, absmax; disagreements mse-l1, mse-absmax, l1-absmax;
+ * summed chosen squared error for mse, l1, absmax} (one CTA per part, fixed
+ * reduction order); the caller folds the parts.
+ */
+int f46_selection_stats(const void* x, int dtype, int64_t rows, int64_t cols, double mcap,
+                        const double* d_amax, double alpha_override, double* d_partials,
+                        int nparts, double* d_alpha_out, f46_stream_t stream);
+
 /* Human-readable build info ("sm_100a ..."). */
 const char* f46_build_info(void);
 

@@ -39,6 +39,7 @@ EXPORTS = (
     "f46_dequantize",
     "f46_gemm_nvfp4",
     "f46_gemm_nvfp4_grouped",
+    "f46_selection_stats",
     "f46_build_info",
 )
 
@@ -65,6 +66,8 @@ def _declare(L):
     L.f46_gemm_nvfp4.restype = i
     L.f46_gemm_nvfp4_grouped.argtypes = [i, p, p, p, p, p, p, i64, i64, i64, p, i64, i, p]
     L.f46_gemm_nvfp4_grouped.restype = i
+    L.f46_selection_stats.argtypes = [p, i, i64, i64, d, p, d, p, i, p, p]
+    L.f46_selection_stats.restype = i
     L.f46_build_info.argtypes = []
     L.f46_build_info.restype = ctypes.c_char_p
 

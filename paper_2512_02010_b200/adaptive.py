@@ -93,21 +93,33 @@ class SelectionStats:
 
 def selection_stats(X, config: QuantConfig, alpha: Optional[float] = None,
                     sr_tag: int = 0) -> SelectionStats:
-    """Per-rule selection statistics (adaptive.py:159-187), from three fused
-    device passes (one per rule) and float64 device reductions."""
+    """Per-rule selection statistics (adaptive.py:159-187) from one fused
+    device pass (f46_selection_stats: exact float64 errors of both candidates,
+    all three rules' picks, counts and chosen squared errors per block)."""
+    from . import _lib
+    from .blockquant import _DT_OF, _check_alpha_override, _stream, _validated_shape, amax_device
+
     _require_adaptive(config)
     _require_plain_nvfp4(config)
+    L = _lib.load()
     t = as_device_tensor(X)
-    picks, agg = {}, {}
-    a = alpha
-    for rule in _RULE_INDEX:
-        q = quantize_1d(t, "adaptive", rule, 256.0, a, want_pick4=True)
-        a = q.alpha if a is None else a
-        picks[rule] = q.pick4.bool()
-        d = dequantize_tensor(q, torch.float64).reshape(-1) - t.reshape(-1).to(torch.float64)
-        agg[rule] = float(torch.sum(d * d) / t.numel())
-    n_blocks = int(picks["mse"].numel())
-    frac = {r: float(p.float().mean()) for r, p in picks.items()}
-    pairs = (("mse", "l1"), ("mse", "absmax"), ("l1", "absmax"))
-    dis = {f"{a_}_vs_{b_}": int((picks[a_] != picks[b_]).sum()) for a_, b_ in pairs}
+    rows, cols = _validated_shape(t)
+    a_over, d_amax = 0.0, None
+    if alpha is not None:
+        a_over = _check_alpha_override(alpha)
+    else:
+        d_amax = amax_device(t)
+        if not bool(torch.isfinite(d_amax).all()):
+            raise InvalidInputError("tensor must be finite")
+    nparts = 4 * torch.cuda.get_device_properties(t.device).multi_processor_count
+    parts = torch.empty((nparts, 9), dtype=torch.float64, device=t.device)
+    rc = L.f46_selection_stats(t.data_ptr(), _DT_OF[t.dtype], rows, cols, 1536.0,
+                               _lib.ptr(d_amax), a_over, parts.data_ptr(), nparts, None, _stream())
+    _lib.check(rc, "f46_selection_stats")
+    tot = parts.sum(dim=0).cpu().numpy()
+    n_blocks = rows * (-(-cols // 16))
+    rules = ("mse", "l1", "absmax")
+    frac = {r: float(tot[i]) / n_blocks for i, r in enumerate(rules)}
+    dis = {"mse_vs_l1": int(tot[3]), "mse_vs_absmax": int(tot[4]), "l1_vs_absmax": int(tot[5])}
+    agg = {r: float(tot[6 + i]) / (rows * cols) for i, r in enumerate(rules)}
     return SelectionStats(n_blocks=n_blocks, fraction_4=frac, disagreements=dis, aggregate_mse=agg)

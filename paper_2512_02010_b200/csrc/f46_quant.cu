@@ -720,6 +720,75 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
 }
 
 // ---------------------------------------------------------------------------
+// Selection statistics for all three rules in one pass (adaptive.py:159-187):
+// per block both candidates' exact float64 errors (sq / abs / max, numpy
+// pairwise order via exact_pass), the 4-vs-6 pick of each rule (strict '<'),
+// counts of 4-picks, pairwise rule disagreements and the chosen candidate's
+// squared error.  Each CTA writes 9 partials (6 counts, 3 sums) in a fixed
+// reduction order, so results are deterministic; the host folds the partials.
+// ---------------------------------------------------------------------------
+template <int DT>
+__global__ void __launch_bounds__(256) stats_kernel(const void* __restrict__ x, int64_t rows,
+                                                    int64_t cols, double mcap, const double* d_amax,
+                                                    double alpha_override, double* partials,
+                                                    double* d_alpha_out) {
+  const int64_t nb = (cols + 15) >> 4;
+  const int64_t total = rows * nb;
+  double alpha = alpha_override;
+  if (!(alpha > 0.0)) {
+    const double amax = *d_amax;
+    alpha = amax == 0.0 ? 1.0 : (double)((float)amax / (float)mcap);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && d_alpha_out) *d_alpha_out = alpha;
+  double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < total;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = b / nb, kb = b - row * nb;
+    double xd[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t c = kb * 16 + i;
+      if (c >= cols)
+        xd[i] = 0.0;
+      else if constexpr (DT == DT_BF16)
+        xd[i] = (double)__uint_as_float(
+            (uint32_t)(reinterpret_cast<const uint16_t*>(x)[row * cols + c]) << 16);
+      else if constexpr (DT == DT_F32)
+        xd[i] = (double)reinterpret_cast<const float*>(x)[row * cols + c];
+      else
+        xd[i] = reinterpret_cast<const double*>(x)[row * cols + c];
+    }
+    ExactPass p6, p4;
+    exact_pass(xd, alpha, 6.0, p6);
+    exact_pass(xd, alpha, 4.0, p4);
+    const bool k_sq = p4.sq < p6.sq, k_ab = p4.ab < p6.ab, k_mx = p4.mx < p6.mx;
+    acc[0] += k_sq;
+    acc[1] += k_ab;
+    acc[2] += k_mx;
+    acc[3] += (k_sq != k_ab);
+    acc[4] += (k_sq != k_mx);
+    acc[5] += (k_ab != k_mx);
+    acc[6] += k_sq ? p4.sq : p6.sq;
+    acc[7] += k_ab ? p4.sq : p6.sq;
+    acc[8] += k_mx ? p4.sq : p6.sq;
+  }
+  __shared__ double red[8][9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 9) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w][threadIdx.x];
+    partials[blockIdx.x * 9 + threadIdx.x] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1: amax
 // ---------------------------------------------------------------------------
 template <int DT>
@@ -1095,6 +1164,31 @@ int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, in
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   quant2d_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
+  return launch_status();
+}
+
+int f46_selection_stats(const void* x, int dtype, int64_t rows, int64_t cols, double mcap,
+                        const double* d_amax, double alpha_override, double* d_partials,
+                        int nparts, double* d_alpha_out, f46_stream_t stream) {
+  if (!x || !d_partials || rows <= 0 || cols <= 0 || nparts < 1) return F46_ERR_INVALID_ARG;
+  if (alpha_override <= 0.0 && (!d_amax || !(mcap > 0.0))) return F46_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (dtype) {
+    case F46_DT_BF16:
+      stats_kernel<DT_BF16><<<nparts, 256, 0, s>>>(x, rows, cols, mcap, d_amax, alpha_override,
+                                                   d_partials, d_alpha_out);
+      break;
+    case F46_DT_F32:
+      stats_kernel<DT_F32><<<nparts, 256, 0, s>>>(x, rows, cols, mcap, d_amax, alpha_override,
+                                                  d_partials, d_alpha_out);
+      break;
+    case F46_DT_F64:
+      stats_kernel<DT_F64><<<nparts, 256, 0, s>>>(x, rows, cols, mcap, d_amax, alpha_override,
+                                                  d_partials, d_alpha_out);
+      break;
+    default:
+      return F46_ERR_INVALID_ARG;
+  }
   return launch_status();
 }
 

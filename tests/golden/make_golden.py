@@ -256,9 +256,47 @@ def linear_cases():
     print(f"wrote {len(names)} linear cases to {path}")
 
 
+def io_and_stats_cases():
+    """Reference NVF4 files (tensor_io.py:136-147) and selection_stats (adaptive.py:159-187)."""
+    import tempfile
+
+    out, names = {}, []
+    cases = [((64, 128), "adaptive", 1), ((33, 20), "fixed6", 2), ((5, 7), "adaptive", 3),
+             ((2, 3, 40), "fixed4", 4), ((16, 30), "adaptive", 5)]
+    for shape, mode, seed in cases:
+        x = bf16(philox(1000 + seed).standard_normal(shape) * 2.0)
+        x64 = bf16_to_f64(x)
+        if mode == "adaptive":
+            cfg = fp4emu.QuantConfig(scale_mode="adaptive")
+            q = fp4emu.quantize_tensor_adaptive(x64, cfg)
+        else:
+            q = fp4emu.quantize_tensor(x64, fp4emu.QuantConfig(scale_mode=mode))
+        with tempfile.NamedTemporaryFile(suffix=".nvf") as fh:
+            fp4emu.write_quantized(fh.name, q)
+            raw = np.frombuffer(open(fh.name, "rb").read(), dtype=np.uint8)
+        name = f"nvf4_{'x'.join(map(str, shape))}_{mode}"
+        names.append(name)
+        rec = dict(x=x, mode=np.array(mode), file=raw)
+        if mode == "adaptive":
+            st = fp4emu.selection_stats(x64, fp4emu.QuantConfig(scale_mode="adaptive"))
+            rec["frac"] = np.array([st.fraction_4[r] for r in ("mse", "l1", "absmax")])
+            rec["dis"] = np.array([st.disagreements[k] for k in ("mse_vs_l1", "mse_vs_absmax", "l1_vs_absmax")])
+            rec["agg"] = np.array([st.aggregate_mse[r] for r in ("mse", "l1", "absmax")])
+            rec["nblocks"] = np.array(st.n_blocks)
+        for k, v in rec.items():
+            out[f"{name}::{k}"] = v
+    out["__names__"] = np.array(names)
+    path = os.path.join(HERE, "golden_io.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(names)} io/stats cases to {path}")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "linear":
         linear_cases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "io":
+        io_and_stats_cases()
     else:
         main()
         linear_cases()
+        io_and_stats_cases()
