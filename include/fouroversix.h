@@ -173,6 +173,28 @@ int f46_selection_stats(const void* x, int dtype, int64_t rows, int64_t cols, do
                         const double* d_amax, double alpha_override, double* d_partials,
                         int nparts, double* d_alpha_out, f46_stream_t stream);
 
+/*
+ * Stochastic-rounding quantization (rounding="sr": blockquant.py:253-257,
+ * codecs.py:120-148), modes as f46_quantize.  key6 / key4 are the Philox4x64
+ * keys of the reference's uniform streams, SeedSequence(seed, spawn_key=(tag,
+ * 6 | 4)).generate_state(2, uint64), derived by the host; the kernel draws
+ * numpy's exact uniforms per element.  Exact float64 arithmetic.
+ */
+int f46_quantize_sr(const void* x, int dtype, int64_t rows, int64_t cols, int mode, int rule,
+                    double mcap, const double* d_amax, double alpha_override, uint64_t key6_0,
+                    uint64_t key6_1, uint64_t key4_0, uint64_t key4_1, uint8_t* codes,
+                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, double* d_alpha_out,
+                    uint32_t* d_flags, f46_stream_t stream);
+
+/*
+ * 16-wide randomized Hadamard transform along the last dim (transforms.py:92-97):
+ * out = fwht(x * signs) / 4 per contiguous group of 16, float64 (numpy's
+ * butterfly order).  n = number of elements (multiple of 16); signs16 is a
+ * HOST array of 16 values +-1.
+ */
+int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double* out,
+              f46_stream_t stream);
+
 /* Human-readable build info ("sm_100a ..."). */
 const char* f46_build_info(void);
 

@@ -40,6 +40,8 @@ EXPORTS = (
     "f46_gemm_nvfp4",
     "f46_gemm_nvfp4_grouped",
     "f46_selection_stats",
+    "f46_quantize_sr",
+    "f46_rht16",
     "f46_build_info",
 )
 
@@ -68,6 +70,11 @@ def _declare(L):
     L.f46_gemm_nvfp4_grouped.restype = i
     L.f46_selection_stats.argtypes = [p, i, i64, i64, d, p, d, p, i, p, p]
     L.f46_selection_stats.restype = i
+    u64 = ctypes.c_uint64
+    L.f46_quantize_sr.argtypes = [p, i, i64, i64, i, i, d, p, d, u64, u64, u64, u64, p, p, p, p, p, p, p]
+    L.f46_quantize_sr.restype = i
+    L.f46_rht16.argtypes = [p, i, i64, p, p, p]
+    L.f46_rht16.restype = i
     L.f46_build_info.argtypes = []
     L.f46_build_info.restype = ctypes.c_char_p
 

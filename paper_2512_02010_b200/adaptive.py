@@ -57,7 +57,8 @@ def quantize_tensor_adaptive(X, config: QuantConfig, alpha: Optional[float] = No
     """
     _require_adaptive(config)
     _require_plain_nvfp4(config)
-    return quantize_1d(X, "adaptive", config.rule, 256.0, alpha, **kw)
+    return quantize_1d(X, "adaptive", config.rule, 256.0, alpha, rounding=config.rounding,
+                       seed=config.seed, sr_tag=sr_tag, **kw)
 
 
 def quantize_block_adaptive(block, alpha: float, rule: str = "mse", rounding: str = "rne",
@@ -101,6 +102,8 @@ def selection_stats(X, config: QuantConfig, alpha: Optional[float] = None,
 
     _require_adaptive(config)
     _require_plain_nvfp4(config)
+    if config.rounding != "rne":
+        raise ConfigError("selection_stats on the B200 path uses rounding='rne'")
     L = _lib.load()
     t = as_device_tensor(X)
     rows, cols = _validated_shape(t)

@@ -40,6 +40,7 @@ __all__ = [
     "quantize_tensor",
     "dequantize_tensor",
     "reconstruction_mse",
+    "sr_keys",
 ]
 
 NVFP4_BLOCK = 16
@@ -343,13 +344,23 @@ def amax_device(t: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Te
     return out
 
 
+def sr_keys(seed: int, sr_tag: int) -> tuple[int, int, int, int]:
+    """Philox4x64 keys of the reference's stochastic-rounding streams
+    (blockquant.py:253-257): SeedSequence(seed, spawn_key=(tag, m)) for m = 6, 4."""
+    k6 = np.random.SeedSequence(entropy=seed, spawn_key=(sr_tag, 6)).generate_state(2, np.uint64)
+    k4 = np.random.SeedSequence(entropy=seed, spawn_key=(sr_tag, 4)).generate_state(2, np.uint64)
+    return int(k6[0]), int(k6[1]), int(k4[0]), int(k4[1])
+
+
 def quantize_1d(X, mode: str, rule: str = "mse", fp8_cap: float = 448.0, alpha=None, *,
                 d_amax: Optional[torch.Tensor] = None, check_finite: bool = True,
-                want_rowmajor: bool = False, want_pick4: bool = False) -> QuantizedTensor:
+                want_rowmajor: bool = False, want_pick4: bool = False,
+                rounding: str = "rne", seed: int = 0, sr_tag: int = 0) -> QuantizedTensor:
     """Quantize X (16-blocks along the last dim) with libfouroversix.
 
     mode  "fixed6" | "fixed4" | "adaptive";  alpha: override (float) or None.
     d_amax: a precomputed (e.g. all-reduced) device amax; else K1 runs here.
+    rounding "sr" draws the reference's Philox uniforms (seed, sr_tag) on the GPU.
     """
     L = _lib.load()
     t = as_device_tensor(X)
@@ -371,11 +382,20 @@ def quantize_1d(X, mode: str, rule: str = "mse", fp8_cap: float = 448.0, alpha=N
         a_over = _check_alpha_override(alpha)
     elif d_amax is None:
         d_amax = amax_device(t)
-    rc = L.f46_quantize(
-        t.data_ptr(), _DT_OF[t.dtype], rows, cols, _lib.MODE[mode], _lib.RULE[rule], mcap,
-        _lib.ptr(d_amax), a_over, codes.data_ptr(), scales_tc.data_ptr(), _lib.ptr(scales_rm),
-        _lib.ptr(pick4), alpha_dev.data_ptr(), flags.data_ptr(), _stream())
-    _lib.check(rc, "f46_quantize")
+    if rounding == "sr":
+        k = sr_keys(seed, sr_tag)
+        rc = L.f46_quantize_sr(
+            t.data_ptr(), _DT_OF[t.dtype], rows, cols, _lib.MODE[mode], _lib.RULE[rule], mcap,
+            _lib.ptr(d_amax), a_over, k[0], k[1], k[2], k[3], codes.data_ptr(),
+            scales_tc.data_ptr(), _lib.ptr(scales_rm), _lib.ptr(pick4), alpha_dev.data_ptr(),
+            flags.data_ptr(), _stream())
+        _lib.check(rc, "f46_quantize_sr")
+    else:
+        rc = L.f46_quantize(
+            t.data_ptr(), _DT_OF[t.dtype], rows, cols, _lib.MODE[mode], _lib.RULE[rule], mcap,
+            _lib.ptr(d_amax), a_over, codes.data_ptr(), scales_tc.data_ptr(), _lib.ptr(scales_rm),
+            _lib.ptr(pick4), alpha_dev.data_ptr(), flags.data_ptr(), _stream())
+        _lib.check(rc, "f46_quantize")
     if check_finite:
         _raise_flags(flags)
     shape = tuple(X.shape) if hasattr(X, "shape") else tuple(t.shape)
@@ -404,9 +424,6 @@ def compute_tensor_scale(X, m_fp4: float, fp8_cap: float) -> float:
 def _require_plain_nvfp4(config: QuantConfig):
     if config.fmt != "nvfp4":
         raise ConfigError("the B200 path implements the nvfp4 format (mxfp4 is out of scope)")
-    if config.rounding != "rne":
-        raise ConfigError("the B200 path implements rounding='rne' (stochastic rounding is a "
-                          "later row of the build plan)")
 
 
 def quantize_tensor(X, config: QuantConfig, alpha: Optional[float] = None, sr_tag: int = 0,
@@ -417,7 +434,8 @@ def quantize_tensor(X, config: QuantConfig, alpha: Optional[float] = None, sr_ta
     if config.sim_hp_scales or config.sim_hp_values or config.threshold is not None:
         raise ConfigError("simulation knobs require quantize_tensor_simulated")
     _require_plain_nvfp4(config)
-    return quantize_1d(X, config.scale_mode, config.rule, config.fp8_cap, alpha, **kw)
+    return quantize_1d(X, config.scale_mode, config.rule, config.fp8_cap, alpha,
+                       rounding=config.rounding, seed=config.seed, sr_tag=sr_tag, **kw)
 
 
 def dequantize_tensor(q: QuantizedTensor, dtype: torch.dtype = torch.float32,

@@ -789,6 +789,215 @@ __global__ void __launch_bounds__(256) stats_kernel(const void* __restrict__ x, 
 }
 
 // ---------------------------------------------------------------------------
+// Stochastic rounding (blockquant.py:253-257 _sr_uniforms, codecs.py:120-148
+// encode_fp4_stochastic) and the 16-wide randomized Hadamard transform
+// (transforms.py:41-105): the gradient recipe of qlinear.py:123-159.
+//
+// Uniforms are numpy's, bit for bit: Generator(Philox(SeedSequence(seed,
+// spawn_key=(tag, m)))).random(shape) is Philox4x64-10 keyed by the
+// SeedSequence's generate_state(2, uint64) (derived on the host), counter
+// value i/4 + 1 for the i-th uint64 of the stream, word i % 4, and the double
+// (x >> 11) * 2^-53.  Element i of the padded block array (rows, nblocks, 16)
+// consumes stream position i, so any schedule gives the same bits.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void philox4x64_10(uint64_t (&c)[4], uint64_t k0, uint64_t k1) {
+  const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// the 16 uniforms of padded block b (stream positions 16b .. 16b+15)
+__device__ __forceinline__ void sr_uniforms16(uint64_t b, uint64_t k0, uint64_t k1, double (&u)[16]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const uint64_t ctr = 4 * b + g + 1;  // 128-bit add would matter only past 2^64 positions
+    uint64_t c[4] = {ctr, 0, 0, 0};
+    philox4x64_10(c, k0, k1);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) u[4 * g + w] = (double)(c[w] >> 11) * 0x1p-53;
+  }
+}
+
+// codecs.py:120-148 for one finite value
+__device__ __forceinline__ uint32_t enc_fp4_sr_d(double x, double u) {
+  const double mags[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  const double xc = fmin(fmax(x, -6.0), 6.0);
+  const double a = fabs(xc);
+  int k = 0;
+#pragma unroll
+  for (int j = 1; j < 8; ++j) k += (mags[j] <= a);
+  if (mags[k] == a) {  // exactly representable: its own code; -0.0 keeps the sign bit
+    if (a == 0.0) return signbit(x) ? 8u : 0u;
+    return (uint32_t)k | (xc < 0.0 ? 8u : 0u);
+  }
+  const double gap = mags[k + 1] - mags[k];
+  if (xc > 0.0) {
+    const bool take_hi = u < (a - mags[k]) / gap;  // (xc - lo) / gap
+    return take_hi ? (uint32_t)(k + 1) : (uint32_t)k;
+  }
+  // negative: lo = -mags[k+1], hi = -mags[k] (0.0 when k == 0, code 0)
+  const bool take_hi = u < (mags[k + 1] - a) / gap;
+  if (take_hi) return k == 0 ? 0u : (8u | (uint32_t)k);
+  return 8u | (uint32_t)(k + 1);
+}
+
+// One fixed-target pass with stochastic rounding (blockquant.py:302-313 with
+// _cast_values' "sr" branch); errors in numpy's pairwise order.
+__device__ __forceinline__ void exact_pass_sr(const double (&x)[16], double alpha, double m,
+                                              const double (&u)[16], ExactPass& o) {
+  double bmax = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) bmax = fmax(bmax, fabs(x[i]));
+  uint32_t sc = enc_e4m3_d(__ddiv_rn(bmax, __dmul_rn(alpha, m)));
+  if (bmax == 0.0) sc = 1;
+  const double denom = __dmul_rn(alpha, dec_e4m3_d(sc));
+  double esq[16], eab[16];
+  double mx = 0.0;
+  uint64_t codes = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double q = denom > 0.0 ? __ddiv_rn(x[i], denom)
+                                 : ((x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0);
+    const uint32_t c = enc_fp4_sr_d(q, u[i]);
+    codes |= (uint64_t)c << (4 * i);
+    const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(c), denom), x[i]);
+    esq[i] = __dmul_rn(diff, diff);
+    eab[i] = fabs(diff);
+    mx = fmax(mx, eab[i]);
+  }
+  o.codes = codes;
+  o.sc = sc;
+  o.sq = pw16(esq);
+  o.ab = pw16(eab);
+  o.mx = mx;
+}
+
+struct SRParams {
+  QParams q;
+  uint64_t k6_0, k6_1, k4_0, k4_1;  // Philox keys of the m=6 / m=4 streams
+};
+
+template <int DT>
+__global__ void __launch_bounds__(128) quant_sr_kernel(SRParams sp) {
+  const QParams& p = sp.q;
+  const int64_t nb = (p.cols + 15) >> 4;
+  const int64_t kb4 = (nb + 3) >> 2;
+  const int64_t rows_pad = (p.rows + 127) & ~(int64_t)127;
+  const int64_t total = rows_pad * kb4 * 4;
+  const double alpha = resolve_alpha(p);
+  prologue_flags(p, alpha);
+  bool nonfinite = false;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / (kb4 * 4), kb = idx - row * (kb4 * 4);
+    if (row >= p.rows || kb >= nb) {
+      p.scales_tc[sf_tc_offset(row, kb, kb4)] = 0;
+      continue;
+    }
+    double xd[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t c = kb * 16 + i;
+      if (c >= p.cols)
+        xd[i] = 0.0;
+      else if constexpr (DT == DT_BF16)
+        xd[i] = (double)__uint_as_float(
+            (uint32_t)(reinterpret_cast<const uint16_t*>(p.x)[row * p.cols + c]) << 16);
+      else if constexpr (DT == DT_F32)
+        xd[i] = (double)reinterpret_cast<const float*>(p.x)[row * p.cols + c];
+      else
+        xd[i] = reinterpret_cast<const double*>(p.x)[row * p.cols + c];
+      nonfinite |= !(fabs(xd[i]) <= 1.7976931348623157e308);
+    }
+    const uint64_t blk = (uint64_t)(row * nb + kb);
+    double u[16];
+    BlockOut o;
+    if (p.mode == ADAPTIVE) {
+      ExactPass p6, p4;
+      sr_uniforms16(blk, sp.k6_0, sp.k6_1, u);
+      exact_pass_sr(xd, alpha, 6.0, u, p6);
+      sr_uniforms16(blk, sp.k4_0, sp.k4_1, u);
+      exact_pass_sr(xd, alpha, 4.0, u, p4);
+      const bool k = rule_err(p4, p.rule) < rule_err(p6, p.rule);
+      o.codes = k ? p4.codes : p6.codes;
+      o.sc = k ? p4.sc : p6.sc;
+      o.pick4 = k;
+    } else {
+      const bool four = p.mode == FIXED4;
+      ExactPass pp;
+      sr_uniforms16(blk, four ? sp.k4_0 : sp.k6_0, four ? sp.k4_1 : sp.k6_1, u);
+      exact_pass_sr(xd, alpha, four ? 4.0 : 6.0, u, pp);
+      o.codes = pp.codes;
+      o.sc = pp.sc;
+      o.pick4 = four;
+    }
+    uint64_t codes = o.codes;
+    const int64_t c0 = kb * 16;
+    if (c0 + 16 > p.cols) {
+      const int valid = (int)(p.cols - c0);
+      codes &= ((1ull << (4 * valid)) - 1);
+    }
+    *reinterpret_cast<uint64_t*>(p.codes + (row * nb + kb) * 8) = codes;
+    p.scales_tc[sf_tc_offset(row, kb, kb4)] = (uint8_t)o.sc;
+    if (p.scales_rm) p.scales_rm[row * nb + kb] = (uint8_t)o.sc;
+    if (p.pick4) p.pick4[row * nb + kb] = (uint8_t)o.pick4;
+  }
+  if (nonfinite && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+}
+
+// transforms.py:92-97 apply_rht: y = fwht(g * signs) / sqrt(16) per group of
+// 16 along the last dim, float64, numpy's butterfly order (h = 1, 2, 4, 8).
+template <int DT>
+__global__ void __launch_bounds__(256) rht16_kernel(const void* __restrict__ x, int64_t ngroups,
+                                                    double4 s0, double4 s1, double4 s2, double4 s3,
+                                                    double* __restrict__ out) {
+  const double sg[16] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w,
+                         s2.x, s2.y, s2.z, s2.w, s3.x, s3.y, s3.z, s3.w};
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    double a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      double v;
+      if constexpr (DT == DT_BF16)
+        v = (double)__uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(x)[g * 16 + i] << 16);
+      else if constexpr (DT == DT_F32)
+        v = (double)reinterpret_cast<const float*>(x)[g * 16 + i];
+      else
+        v = reinterpret_cast<const double*>(x)[g * 16 + i];
+      a[i] = __dmul_rn(v, sg[i]);
+    }
+#pragma unroll
+    for (int h = 1; h < 16; h <<= 1) {
+      double b[16];
+#pragma unroll
+      for (int blk = 0; blk < 16; blk += 2 * h)
+#pragma unroll
+        for (int j = 0; j < h; ++j) {
+          b[blk + j] = __dadd_rn(a[blk + j], a[blk + h + j]);
+          b[blk + h + j] = __dsub_rn(a[blk + j], a[blk + h + j]);
+        }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = b[i];
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) out[g * 16 + i] = __ddiv_rn(a[i], 4.0);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1: amax
 // ---------------------------------------------------------------------------
 template <int DT>
@@ -806,7 +1015,21 @@ __global__ void __launch_bounds__(256) amax_kernel(const void* __restrict__ x, i
       const int64_t nv = n >> 3;
       const uint4* xv = reinterpret_cast<const uint4*>(x);
       uint32_t m = 0;
-      for (int64_t i = tid; i < nv; i += stride) {
+      int64_t i = tid;
+      // four independent 16-byte loads in flight per thread
+      for (; i + 3 * stride < nv; i += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldcs(xv + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          m = __vmaxu2(m, v[u].x & 0x7FFF7FFFu);
+          m = __vmaxu2(m, v[u].y & 0x7FFF7FFFu);
+          m = __vmaxu2(m, v[u].z & 0x7FFF7FFFu);
+          m = __vmaxu2(m, v[u].w & 0x7FFF7FFFu);
+        }
+      }
+      for (; i < nv; i += stride) {
         const uint4 v = __ldcs(xv + i);
         m = __vmaxu2(m, v.x & 0x7FFF7FFFu);
         m = __vmaxu2(m, v.y & 0x7FFF7FFFu);
@@ -1185,6 +1408,68 @@ int f46_selection_stats(const void* x, int dtype, int64_t rows, int64_t cols, do
     case F46_DT_F64:
       stats_kernel<DT_F64><<<nparts, 256, 0, s>>>(x, rows, cols, mcap, d_amax, alpha_override,
                                                   d_partials, d_alpha_out);
+      break;
+    default:
+      return F46_ERR_INVALID_ARG;
+  }
+  return launch_status();
+}
+
+int f46_quantize_sr(const void* x, int dtype, int64_t rows, int64_t cols, int mode, int rule,
+                    double mcap, const double* d_amax, double alpha_override, uint64_t key6_0,
+                    uint64_t key6_1, uint64_t key4_0, uint64_t key4_1, uint8_t* codes,
+                    uint8_t* scales_tc, uint8_t* scales_rm, uint8_t* pick4, double* d_alpha_out,
+                    uint32_t* d_flags, f46_stream_t stream) {
+  if (!x || !codes || !scales_tc || rows <= 0 || cols <= 0) return F46_ERR_INVALID_ARG;
+  if (mode < F46_FIXED6 || mode > F46_ADAPTIVE || rule < F46_RULE_MSE || rule > F46_RULE_ABSMAX)
+    return F46_ERR_CONFIG;
+  if (alpha_override <= 0.0 && (!d_amax || !(mcap > 0.0))) return F46_ERR_INVALID_ARG;
+  SRParams sp{{x, rows, cols, mode, rule, dtype, mcap, d_amax, alpha_override, codes, scales_tc,
+               scales_rm, pick4, d_alpha_out, d_flags},
+              key6_0, key6_1, key4_0, key4_1};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nb = (cols + 15) / 16;
+  const int64_t total = ((rows + 127) & ~(int64_t)127) * (((nb + 3) / 4) * 4);
+  int64_t grid = (total + 127) / 128;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (grid > cap) grid = cap;
+  switch (dtype) {
+    case F46_DT_BF16:
+      quant_sr_kernel<DT_BF16><<<(unsigned)grid, 128, 0, s>>>(sp);
+      break;
+    case F46_DT_F32:
+      quant_sr_kernel<DT_F32><<<(unsigned)grid, 128, 0, s>>>(sp);
+      break;
+    case F46_DT_F64:
+      quant_sr_kernel<DT_F64><<<(unsigned)grid, 128, 0, s>>>(sp);
+      break;
+    default:
+      return F46_ERR_INVALID_ARG;
+  }
+  return launch_status();
+}
+
+int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double* out,
+              f46_stream_t stream) {
+  if (!x || !signs16 || !out || n <= 0 || n % 16) return F46_ERR_INVALID_ARG;
+  const double* g = signs16;
+  const double4 s0 = make_double4(g[0], g[1], g[2], g[3]), s1 = make_double4(g[4], g[5], g[6], g[7]);
+  const double4 s2 = make_double4(g[8], g[9], g[10], g[11]),
+                s3 = make_double4(g[12], g[13], g[14], g[15]);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ng = n / 16;
+  int64_t grid = (ng + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (grid > cap) grid = cap;
+  switch (dtype) {
+    case F46_DT_BF16:
+      rht16_kernel<DT_BF16><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
+      break;
+    case F46_DT_F32:
+      rht16_kernel<DT_F32><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
+      break;
+    case F46_DT_F64:
+      rht16_kernel<DT_F64><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
       break;
     default:
       return F46_ERR_INVALID_ARG;

@@ -155,8 +155,24 @@ def linear_dgrad(dy, W, config, *, bf16_out: bool = False) -> torch.Tensor:
     return emulated_fp4_matmul(dyq, wq.transposed, transpose_b=True, bf16_out=bf16_out)
 
 
-def linear_wgrad(dy, x, config, *, bf16_out: bool = False):
-    """dW = q(T dy)^T @ q(T x) (qlinear.py:138-159) needs the randomized
-    Hadamard transform along the batch, which is not on the B200 path yet."""
-    raise ConfigError("linear_wgrad needs the randomized Hadamard transform (SURVEY.md 8(f) "
-                      "row 2), not implemented on the B200 path yet")
+def linear_wgrad(dy, x, config, *, bf16_out: bool = False) -> torch.Tensor:
+    """dW = q(T dy)^T @ q(T x) (qlinear.py:138-159): both operands pass
+    through the 16-wide randomized Hadamard transform along the batch axis
+    (f46_rht16, float64), are quantized along it with the configured rounding
+    (stochastic: numpy-exact Philox uniforms, tags 2 and 3), and meet in a
+    K-major tcgen05 GEMM contracting over the batch."""
+    from .blockquant import as_device_tensor
+    from .transforms import RhtSpec, apply_rht
+
+    _check_2d("dy", dy)
+    _check_2d("x", x)
+    if dy.shape[0] != x.shape[0]:
+        raise InvalidInputError("dy and x disagree on the batch dimension")
+    spec = RhtSpec(seed=config.seed)
+    if dy.shape[0] % spec.size:
+        raise InvalidInputError(f"batch dimension must be a multiple of {spec.size} for wgrad")
+    a = apply_rht(as_device_tensor(dy).T.contiguous(), spec)  # (out, batch)
+    b = apply_rht(as_device_tensor(x).T.contiguous(), spec)   # (in, batch)
+    aq = _quantize_1d(a, config, sr_tag=2)
+    bq = _quantize_1d(b, config, sr_tag=3)
+    return emulated_fp4_matmul(aq, bq, transpose_b=True, bf16_out=bf16_out)

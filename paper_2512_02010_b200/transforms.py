@@ -8,8 +8,12 @@ same pass also yields W^T as an NVFP4 tensor blocked along W's rows; it is
 attached as ``q.transposed`` and is what ``linear_dgrad``'s GEMM consumes
 (qlinear.py:123-135: dy @ W needs W blocked along `out`).
 
-The randomized Hadamard transform (transforms.py:41-105) belongs to the
-gradient recipe and is not on the B200 path yet.
+``RhtSpec`` / ``apply_rht`` / ``invert_rht`` mirror the randomized Hadamard
+transform of the gradient recipe (transforms.py:41-105): the sign diagonal is
+drawn on the host exactly as the reference draws it (numpy Philox from
+SeedSequence(seed, spawn_key=(0x5D,)) -- a 16-entry parameter), and the
+transform itself runs in the f46_rht16 kernel in float64 with numpy's
+butterfly order, so its output is bit-identical to the reference's.
 """
 
 from __future__ import annotations
@@ -33,9 +37,63 @@ from .blockquant import (
 )
 from .errors import ConfigError, InvalidInputError
 
-__all__ = ["TILE", "quantize_weights_2d"]
+__all__ = ["TILE", "RhtSpec", "apply_rht", "invert_rht", "quantize_weights_2d"]
 
 TILE = 16
+_SIGN_TAG = 0x5D  # transforms.py:38
+
+
+class RhtSpec:
+    """Transform parameters (transforms.py:44-67); signs derive from the seed
+    unless given."""
+
+    def __init__(self, size: int = 16, seed: int = 0, signs=None):
+        if size < 1 or size & (size - 1):
+            raise ConfigError("transform size must be a power of two")
+        self.size = size
+        self.seed = seed
+        if signs is None:
+            ss = np.random.SeedSequence(entropy=seed, spawn_key=(_SIGN_TAG,))
+            rng = np.random.Generator(np.random.Philox(ss))
+            signs = rng.integers(0, 2, size=size) * 2.0 - 1.0
+        else:
+            signs = np.asarray(signs, dtype=np.float64)
+            if signs.shape != (size,) or not np.isin(signs, (-1.0, 1.0)).all():
+                raise ConfigError("signs must be +-1 and match size")
+        self.signs = np.ascontiguousarray(signs, dtype=np.float64)
+
+
+def _rht_kernel(t: torch.Tensor, signs: np.ndarray) -> torch.Tensor:
+    L = _lib.load()
+    out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
+    sg = np.ascontiguousarray(signs, dtype=np.float64)
+    rc = L.f46_rht16(t.data_ptr(), _DT_OF[t.dtype], t.numel(), sg.ctypes.data, out.data_ptr(),
+                     _stream())
+    _lib.check(rc, "f46_rht16")
+    return out
+
+
+def _grouped(X, size: int) -> torch.Tensor:
+    t = as_device_tensor(X)
+    if t.dim() == 0 or t.shape[-1] % size:
+        raise InvalidInputError(f"last dimension must be a positive multiple of {size}")
+    if size != 16:
+        raise ConfigError("the B200 transform kernel is the 16-wide one")
+    return t.contiguous()
+
+
+def apply_rht(X, spec: RhtSpec) -> torch.Tensor:
+    """y = fwht(g * signs) / sqrt(16) per group of 16 along the last dim
+    (transforms.py:92-97); float64 CUDA tensor."""
+    return _rht_kernel(_grouped(X, spec.size), spec.signs)
+
+
+def invert_rht(Y, spec: RhtSpec) -> torch.Tensor:
+    """x = (fwht(g) / sqrt(16)) * signs (transforms.py:100-105)."""
+    t = _grouped(Y, spec.size)
+    y = _rht_kernel(t, np.ones(spec.size))
+    sg = torch.from_numpy(spec.signs).to(y.device)
+    return (y.reshape(-1, spec.size) * sg).reshape(y.shape)
 
 
 def quantize_weights_2d(W, config: QuantConfig, alpha: Optional[float] = None, sr_tag: int = 0,

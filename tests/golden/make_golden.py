@@ -291,8 +291,53 @@ def io_and_stats_cases():
     print(f"wrote {len(names)} io/stats cases to {path}")
 
 
+def sr_rht_cases():
+    """Stochastic rounding (blockquant.py:253-257), the RHT (transforms.py:92-105)
+    and the gradient recipes with rounding='sr' (qlinear.py:123-159)."""
+    out, names = {}, []
+
+    def put(name, **rec):
+        names.append(name)
+        for k, v in rec.items():
+            out[f"{name}::{k}"] = v
+
+    for i, (shape, mode, seed, tag) in enumerate([((64, 128), "adaptive", 5, 1),
+                                                   ((33, 40), "fixed6", 7, 2),
+                                                   ((16, 48), "fixed4", 0, 3),
+                                                   ((128, 256), "adaptive", 11, 0)]):
+        x = bf16(philox(1100 + i).standard_normal(shape))
+        cfg = fp4emu.QuantConfig(scale_mode=mode, rounding="sr", seed=seed)
+        x64 = bf16_to_f64(x)
+        if mode == "adaptive":
+            q = fp4emu.quantize_tensor_adaptive(x64, cfg, sr_tag=tag)
+        else:
+            q = fp4emu.quantize_tensor(x64, cfg, sr_tag=tag)
+        put(f"sr_{'x'.join(map(str, shape))}_{mode}_s{seed}_t{tag}", x=x, mode=np.array(mode),
+            seed=np.array(seed), tag=np.array(tag), alpha=np.array(q.alpha),
+            scales=np.asarray(q.scale_codes, np.uint8), codes=pack_codes(np.asarray(q.codes).reshape(shape[0], -1)))
+    for i, seed in enumerate((0, 5)):
+        x = philox(1200 + i).standard_normal((24, 64))
+        spec = fp4emu.RhtSpec(seed=seed)
+        put(f"rht_s{seed}", x=x, seed=np.array(seed), y=fp4emu.apply_rht(x, spec),
+            inv=fp4emu.invert_rht(x, spec))
+    for i, (B, IN, OUT, mode) in enumerate([(32, 64, 48, "adaptive"), (48, 96, 80, "fixed6")]):
+        x = bf16(philox(1300 + i).standard_normal((B, IN)))
+        W = bf16(philox(1350 + i).standard_normal((OUT, IN)) * 0.05)
+        dy = bf16(philox(1380 + i).standard_normal((B, OUT)))
+        cfg = fp4emu.QuantConfig(scale_mode=mode, rounding="sr", seed=3)
+        dx = fp4emu.linear_dgrad(bf16_to_f64(dy), bf16_to_f64(W), cfg)
+        dw = fp4emu.linear_wgrad(bf16_to_f64(dy), bf16_to_f64(x), cfg)
+        put(f"grad_{B}x{IN}x{OUT}_{mode}", x=x, W=W, dy=dy, dx=dx, dw=dw, mode=np.array(mode))
+    out["__names__"] = np.array(names)
+    path = os.path.join(HERE, "golden_sr.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(names)} sr/rht cases to {path}")
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "linear":
+    if len(sys.argv) > 1 and sys.argv[1] == "sr":
+        sr_rht_cases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "linear":
         linear_cases()
     elif len(sys.argv) > 1 and sys.argv[1] == "io":
         io_and_stats_cases()
@@ -300,3 +345,4 @@ if __name__ == "__main__":
         main()
         linear_cases()
         io_and_stats_cases()
+        sr_rht_cases()

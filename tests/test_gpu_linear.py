@@ -96,8 +96,3 @@ def test_dgrad_gemm_is_tensor_core_transpose_product():
     wq = f46.quantize_weights_2d(x.cuda(), cfg)
     ref = f46.dequantize_tensor(dyq, torch.float64) @ f46.dequantize_tensor(wq, torch.float64)
     assert rel_fro(dx, ref) <= REL_TOL
-
-
-def test_wgrad_not_on_b200_path():
-    with pytest.raises(f46.ConfigError):
-        f46.linear_wgrad(torch.ones(16, 16), torch.ones(16, 16), f46.QuantConfig())

@@ -35,4 +35,15 @@ for i in range(25):
         ts.append(a.elapsed_time(b))
 ms = sum(ts) / len(ts)
 bpe = (2 if dt == "bf16" else 4) + 0.5625
-print(f"{os.path.basename(os.environ.get('F46_LIB_PATH', 'default'))} {mode} {dt}: K2 {ms*1e3:.1f} us  {rows*cols*bpe/ms/1e6:.0f} GB/s")
+ta = []
+for i in range(25):
+    flush.fill_(i)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    L.f46_amax(x.data_ptr(), DT, x.numel(), amax.data_ptr(), s)
+    b.record()
+    torch.cuda.synchronize()
+    if i >= 5:
+        ta.append(a.elapsed_time(b))
+ma = sum(ta) / len(ta)
+print(f"{os.path.basename(os.environ.get('F46_LIB_PATH', 'default'))} {mode} {dt}: K2 {ms*1e3:.1f} us  {rows*cols*bpe/ms/1e6:.0f} GB/s | K1 amax {ma*1e3:.1f} us {rows*cols*(bpe-0.5625)/ma/1e6:.0f} GB/s")
