@@ -1096,9 +1096,11 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
   const bool f32_alpha = ((double)alpha == alpha_d);
   const int64_t total = rows * nb;
   bool nan_scale = false;
+  const bool small = total < (1ll << 32);
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = idx / nb, kb = idx - row * nb;
+    const int64_t row = small ? (int64_t)((uint32_t)idx / (uint32_t)nb) : idx / nb;
+    const int64_t kb = idx - row * nb;
     const uint32_t sc = SL == F46_SCALES_TC ? scales[sf_tc_offset(row, kb, kb4)] : scales[idx];
     nan_scale |= ((sc & 0x7F) == 0x7F);
     const uint64_t cw = *reinterpret_cast<const uint64_t*>(codes + idx * 8);
@@ -1113,6 +1115,67 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
         const double v = __dmul_rn(__dmul_rn(dec_fp4_d((uint32_t)(cw >> (4 * i)) & 15u), alpha_d),
                                    delta);
         if (c0 + i < cols) o[i] = v;
+      }
+    } else if (f32_alpha) {
+      // hardware decode: E2M1 pairs -> f16x2 -> f32 (exact), v*Delta exact in
+      // f32 (<= 6 significant bits), one rounding of (v*Delta)*alpha
+      const float delta = e4m3_to_f32(sc & 0x7F) * ((sc & 0x80) ? -1.f : 1.f);
+      const float2 d2 = make_float2(delta, delta), a2 = make_float2(alpha, alpha);
+      float y[16];
+      const uint32_t cwl = (uint32_t)cw, cwh = (uint32_t)(cw >> 32);
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp) {
+        const uint32_t w = pp < 4 ? cwl : cwh;
+        uint32_t h;
+        switch (pp & 3) {
+          case 0: { const __half2 t = e2m1x2_to_h2<0>(w); h = *reinterpret_cast<const uint32_t*>(&t); } break;
+          case 1: { const __half2 t = e2m1x2_to_h2<1>(w); h = *reinterpret_cast<const uint32_t*>(&t); } break;
+          case 2: { const __half2 t = e2m1x2_to_h2<2>(w); h = *reinterpret_cast<const uint32_t*>(&t); } break;
+          default: { const __half2 t = e2m1x2_to_h2<3>(w); h = *reinterpret_cast<const uint32_t*>(&t); } break;
+        }
+        const float2 v = make_float2(fhadd_h<0>(h, -0.f), fhadd_h<1>(h, -0.f));
+        const float2 vd = __fmul2_rn(v, d2);
+        if constexpr (OUT == DT_F32) {
+          const float2 r = __fmul2_rn(vd, a2);
+          y[2 * pp] = r.x;
+          y[2 * pp + 1] = r.y;
+        } else {
+          // round-to-odd to f32, then RN to bf16 == one rounding of the exact product
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const float vv = e ? vd.y : vd.x;
+            const float rz = __fmul_rz(vv, alpha);
+            const float rem = fmaf(vv, alpha, -rz);
+            y[2 * pp + e] = __uint_as_float(__float_as_uint(rz) | (rem != 0.f ? 1u : 0u));
+          }
+        }
+      }
+      if constexpr (OUT == DT_F32) {
+        float* o = reinterpret_cast<float*>(out) + row * cols + c0;
+        if (full && ((((uintptr_t)o) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            reinterpret_cast<float4*>(o)[q] =
+                make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+        } else {
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < cols) o[i] = y[i];
+        }
+      } else {
+        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + row * cols + c0;
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const __nv_bfloat162 hb = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
+          w[q] = *reinterpret_cast<const uint32_t*>(&hb);
+        }
+        if (full && ((((uintptr_t)o) & 15) == 0)) {
+          reinterpret_cast<uint4*>(o)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+          reinterpret_cast<uint4*>(o)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        } else {
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < cols) reinterpret_cast<uint16_t*>(o)[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+        }
       }
     } else {
       const float delta = e4m3_to_f32(sc & 0x7F) * ((sc & 0x80) ? -1.f : 1.f);
@@ -1172,6 +1235,94 @@ __global__ void __launch_bounds__(256) dequant_kernel(const uint8_t* __restrict_
             }
         }
       }
+    }
+  }
+  if (nan_scale && d_flags) atomicOr(d_flags, F46_FLAG_NAN_SCALE);
+}
+
+// Coalesced K3 for f32 / bf16 output with a float32 alpha: each thread owns EPT
+// consecutive elements (16 bytes of output), so a warp's store instruction
+// covers 512 contiguous bytes; the block's scale byte is shared by 16/EPT
+// neighbouring threads.  Same arithmetic as dequant_kernel's fast branch.
+template <int OUT, int SL>
+__global__ void __launch_bounds__(256) dequant_vec_kernel(const uint8_t* __restrict__ codes,
+                                                          const uint8_t* __restrict__ scales,
+                                                          const double* d_alpha, int64_t rows,
+                                                          int64_t cols, void* out,
+                                                          uint32_t* d_flags) {
+  constexpr int EPT = OUT == DT_F32 ? 4 : 8;  // 16 output bytes per thread
+  constexpr int TPB = 16 / EPT;                // threads per 16-element block
+  const int64_t nb = cols >> 4;                // cols % 16 == 0 on this path
+  const int64_t kb4 = (nb + 3) >> 2;
+  const double alpha_d = *d_alpha;
+  const float alpha = (float)alpha_d;
+  const bool f32_alpha = (double)alpha == alpha_d;  // else: float64 product, one rounding
+  const int64_t total = rows * nb * TPB;
+  const bool small = rows * nb < (1ll << 32);
+  bool nan_scale = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = t / TPB;
+    const int part = (int)(t % TPB);
+    const int64_t row = small ? (int64_t)((uint32_t)idx / (uint32_t)nb) : idx / nb;
+    const int64_t kb = idx - row * nb;
+    const uint32_t sc = SL == F46_SCALES_TC ? scales[sf_tc_offset(row, kb, kb4)] : scales[idx];
+    nan_scale |= ((sc & 0x7F) == 0x7F);
+    const float delta = e4m3_to_f32(sc & 0x7F) * ((sc & 0x80) ? -1.f : 1.f);
+    const float2 d2 = make_float2(delta, delta), a2 = make_float2(alpha, alpha);
+    uint32_t w;  // EPT codes, even element in the low nibble
+    if (EPT == 4)
+      w = *reinterpret_cast<const uint16_t*>(codes + idx * 8 + part * 2);
+    else
+      w = *reinterpret_cast<const uint32_t*>(codes + idx * 8 + part * 4);
+    float y[EPT];
+#pragma unroll
+    for (int pp = 0; pp < EPT / 2; ++pp) {
+      uint32_t h;
+      switch (pp) {
+        case 0: { const __half2 q = e2m1x2_to_h2<0>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+        case 1: { const __half2 q = e2m1x2_to_h2<1>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+        case 2: { const __half2 q = e2m1x2_to_h2<2>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+        default: { const __half2 q = e2m1x2_to_h2<3>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+      }
+      const float2 vd = __fmul2_rn(make_float2(fhadd_h<0>(h, -0.f), fhadd_h<1>(h, -0.f)), d2);
+      if (!f32_alpha) {
+        // (vals * alpha) * scale in float64 exactly as blockquant.py:376, one rounding
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const double d = __dmul_rn((double)(e ? vd.y : vd.x), alpha_d);
+          if constexpr (OUT == DT_F32) {
+            y[2 * pp + e] = __double2float_rn(d);
+          } else {
+            const float rz = __double2float_rz(d);
+            y[2 * pp + e] = __uint_as_float(__float_as_uint(rz) | ((double)rz != d ? 1u : 0u));
+          }
+        }
+      } else if constexpr (OUT == DT_F32) {
+        const float2 r = __fmul2_rn(vd, a2);
+        y[2 * pp] = r.x;
+        y[2 * pp + 1] = r.y;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float vv = e ? vd.y : vd.x;
+          const float rz = __fmul_rz(vv, alpha);
+          const float rem = fmaf(vv, alpha, -rz);
+          y[2 * pp + e] = __uint_as_float(__float_as_uint(rz) | (rem != 0.f ? 1u : 0u));
+        }
+      }
+    }
+    const int64_t e0 = row * cols + kb * 16 + part * EPT;
+    if constexpr (OUT == DT_F32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + e0) = make_float4(y[0], y[1], y[2], y[3]);
+    } else {
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162 hb = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
+        o[q] = *reinterpret_cast<const uint32_t*>(&hb);
+      }
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out) + e0) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
   if (nan_scale && d_flags) atomicOr(d_flags, F46_FLAG_NAN_SCALE);
@@ -1347,9 +1498,26 @@ int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout
   int64_t grid = (total + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
+  const bool tc = scale_layout == F46_SCALES_TC;
+  // coalesced path: f32 / bf16 out, cols % 16 == 0, 16-byte aligned rows
+  if ((out_dtype == F46_DT_F32 || out_dtype == F46_DT_BF16) && cols % 16 == 0 &&
+      (((uintptr_t)out) & 15) == 0 && (((uintptr_t)codes) & 3) == 0) {
+    const int tpb = out_dtype == F46_DT_F32 ? 4 : 2;
+    int64_t g2 = (total * tpb + 255) / 256;
+    const int64_t cap2 = (int64_t)num_sms() * 16;
+    if (g2 > cap2) g2 = cap2;
+#define F46_DQV(OUT, SL) \
+  dequant_vec_kernel<OUT, SL><<<(unsigned)g2, 256, 0, s>>>(codes, scales, d_alpha, rows, cols, out, d_flags)
+    if (out_dtype == F46_DT_F32) {
+      if (tc) F46_DQV(DT_F32, F46_SCALES_TC); else F46_DQV(DT_F32, F46_SCALES_RM);
+    } else {
+      if (tc) F46_DQV(DT_BF16, F46_SCALES_TC); else F46_DQV(DT_BF16, F46_SCALES_RM);
+    }
+#undef F46_DQV
+    return launch_status();
+  }
 #define F46_DQ(OUT, SL) \
   dequant_kernel<OUT, SL><<<(unsigned)grid, 256, 0, s>>>(codes, scales, d_alpha, rows, cols, out, d_flags)
-  const bool tc = scale_layout == F46_SCALES_TC;
   switch (out_dtype) {
     case F46_DT_F32:
       if (tc) F46_DQ(DT_F32, F46_SCALES_TC); else F46_DQ(DT_F32, F46_SCALES_RM);

@@ -47,3 +47,20 @@ for i in range(25):
         ta.append(a.elapsed_time(b))
 ma = sum(ta) / len(ta)
 print(f"{os.path.basename(os.environ.get('F46_LIB_PATH', 'default'))} {mode} {dt}: K2 {ms*1e3:.1f} us  {rows*cols*bpe/ms/1e6:.0f} GB/s | K1 amax {ma*1e3:.1f} us {rows*cols*(bpe-0.5625)/ma/1e6:.0f} GB/s")
+# K3 dequantize of the same tensor (bf16 and f32 out)
+alpha = torch.tensor([0.003], dtype=torch.float64, device=dev)
+for od, dtc, ob in ((torch.bfloat16, _lib.DT_BF16, 2), (torch.float32, _lib.DT_F32, 4)):
+    out = torch.empty((rows, cols), dtype=od, device=dev)
+    td = []
+    for i in range(15):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        L.f46_dequantize(codes.data_ptr(), scales.data_ptr(), 0, alpha.data_ptr(), rows, cols,
+                         out.data_ptr(), dtc, None, s)
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 5:
+            td.append(a.elapsed_time(b))
+    md = sum(td) / len(td)
+    print(f"  K3 dequant -> {od}: {md*1e3:.1f} us  {rows*cols*(0.5625+ob)/md/1e6:.0f} GB/s")
