@@ -322,6 +322,7 @@ def run_b200(args):
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_extras:
+        line["dequant"] = bench_dequant(args, L, dev, peaks, codes, scales, alpha, rows_local)
         line["weights"] = bench_weights(args, L, dev, peaks)
         line["gemm"] = bench_gemm(args, dev, peaks)
         line["moe"] = bench_moe(args, dev)
@@ -331,6 +332,36 @@ def run_b200(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_dequant(args, L, dev, peaks, codes, scales, alpha, rows):
+    """K3: dequantize the c3 tensor's codes back to bf16 / f32 (L2 flushed)."""
+    import torch
+
+    from paper_2512_02010_b200 import _lib
+
+    stream = torch.cuda.current_stream()
+    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out = {}
+    for od, code, ob in ((torch.bfloat16, _lib.DT_BF16, 2), (torch.float32, _lib.DT_F32, 4)):
+        y = torch.empty((rows, COLS), dtype=od, device=dev)
+        ts = []
+        for i in range(max(5, args.steps) + 3):
+            flush_buf.fill_(i & 0xFF)
+            s, e = _events(2)
+            s.record(stream)
+            _lib.check(L.f46_dequantize(codes.data_ptr(), scales.data_ptr(), _lib.SCALES_TC,
+                                        alpha.data_ptr(), rows, COLS, y.data_ptr(), code, None,
+                                        stream.cuda_stream), "dequantize")
+            e.record(stream)
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(s.elapsed_time(e))
+        ms = sum(ts) / len(ts)
+        gbs = rows * COLS * (0.5625 + ob) / (ms * 1e-3) / 1e9
+        out[str(od).split(".")[-1]] = {"ms": ms, "GB/s": gbs, "frac_of_hbm": gbs / peaks["hbm_gbs"],
+                                       "bytes_per_elem": 0.5625 + ob}
+    return out
 
 
 def bench_weights(args, L, dev, peaks):
@@ -442,9 +473,9 @@ def bench_gemm(args, dev, peaks):
 def bench_moe(args, dev):
     """Config 5 (per GPU of an 8-GPU EP job): Nemotron-3-Nano experts, hidden
     2688, FFN 1856, 3072 tokens per expert, 16 experts per GPU.  FPROP (x W1^T,
-    h W2^T) and WGRAD (dh^T x, dy^T h; contraction over tokens) as grouped
-    NVFP4 GEMMs of 4/6-quantized operands.  DGRAD needs W^T blocked along the
-    output dim (2-D tile quantization, a later row) and is not timed."""
+    h W2^T), DGRAD (dh W1, dy W2: against the W^T containers of the 2-D tile
+    quantizer) and WGRAD (dh^T x, dy^T h; contraction over tokens) as grouped
+    NVFP4 GEMMs of 4/6-quantized operands."""
     import torch
 
     import paper_2512_02010_b200 as f46
@@ -460,9 +491,19 @@ def bench_moe(args, dev):
         return (torch.stack([q.packed_codes for q in qs]), torch.stack([q.scales_tc for q in qs]),
                 torch.cat([q.alpha_dev for q in qs]))
 
+    def wstack_t(rows, cols):
+        # 2-D 16x16-tile weights (transforms.py:134-179): W^T is K-major along `out`
+        qs = [f46.quantize_weights_2d(
+            (torch.randn(rows, cols, generator=g, device=dev) * 0.02).to(torch.bfloat16), cfg,
+            check_finite=False).transposed for _ in range(E)]
+        return (torch.stack([q.packed_codes for q in qs]), torch.stack([q.scales_tc for q in qs]),
+                torch.cat([q.alpha_dev for q in qs]))
+
     gemms = {
         "fprop_x_w1": (qstack(T, H, 1.0), qstack(F, H, 0.02), T, F, H),
         "fprop_h_w2": (qstack(T, F, 1.0), qstack(H, F, 0.02), T, H, F),
+        "dgrad_dh_w1": (qstack(T, F, 1e-3), wstack_t(F, H), T, H, F),
+        "dgrad_dy_w2": (qstack(T, H, 1e-3), wstack_t(H, F), T, F, H),
         "wgrad_dh_x": (qstack(F, T, 1e-3), qstack(H, T, 1.0), F, H, T),
         "wgrad_dy_h": (qstack(H, T, 1e-3), qstack(F, T, 1.0), H, F, T),
     }

@@ -1,10 +1,12 @@
-# Full GPU check: tests, bench (N=1), launch list, ncu captures of K2 and the GEMM.
+# Full GPU check: tests, bench (N=1), reference arm, launch list, ncu captures of K2, the GEMM and K3.
 set -x
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
 cat gpurun_out/bench.json
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-extras > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:quant_seg -c 1 -o gpurun_out/quant_full python tools/prof_quant.py > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm_nvfp4 -s 3 -c 1 -o gpurun_out/gemm_full python tools/time_gemm.py 8192 8192 8192 bf16 > /dev/null 2>&1
+DEQ=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dequant -c 1 -o gpurun_out/dequant_full python tools/prof_quant.py > /dev/null 2>&1
+timeout 300 python tools/gemm_clock.py
 ls gpurun_out
