@@ -458,13 +458,13 @@ def bench_gemm(args, dev, peaks):
     return {
         "metric": "4/6-NVFP4 GEMM TFLOP/s", "shape": [M, N, K], "value": tf, "unit": "TFLOP/s",
         "out": out,
-        "roofline": {"bound": "tensor", "kernel": "gemm_nvfp4_persistent<bf16>",
+        "roofline": {"bound": "tensor", "kernel": "gemm_nvfp4_pair<bf16> (tcgen05 cta_group::2)",
                      "achieved": tf, "peak": FP4_DENSE_NOMINAL_TFLOPS,
                      "peak_kind": "nominal dense FP4 (no measured FP4 peak on this pool)",
                      "unit": "TFLOP/s", "frac": tf / FP4_DENSE_NOMINAL_TFLOPS,
                      "frac_vs_4x_measured_bf16": tf / fp4_from_bf16,
                      "algorithmic_flops_per_launch": flops, "launch_ms": out["bf16"]["ms"],
-                     "traffic": profile_traffic("gemm_nvfp4_persistent")},
+                     "traffic": profile_traffic("gemm_nvfp4_pair")},
         "quantize_a_b_plus_gemm_ms": full_ms,
         "data": "synthetic N(0,1) bf16 operands, both quantized with 4/6 (adaptive)",
     }

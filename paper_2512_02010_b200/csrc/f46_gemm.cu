@@ -28,6 +28,7 @@
 #include <stdio.h>
 
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <mutex>
@@ -474,13 +475,25 @@ __global__ void __launch_bounds__(kThreadsP, 1)
 // through the slower, MMA-serialised copy path (tools/mma_rate.cu: 12 copies
 // per 4 MMAs cost 86 extra cycles per MMA).
 // ---------------------------------------------------------------------------
-constexpr int kStagesPair = 5;
+// bf16 output goes through a 32 KB smem staging area and TMA stores, so the
+// accumulator is released before any global store is issued (stores issued
+// ahead of the release stalled it: 221 -> 180 us when compiled out).  Each
+// epilogue warp stages the first 64 of its 128 columns, keeps the other 64
+// packed in registers, releases TMEM, then stores the two boxes in turn.
+template <int OUT_BF16>
+struct PairCfg {
+  static constexpr int kStages = 5;
+  static constexpr int kStaging = OUT_BF16 ? 8 * 4096 : 0;  // 8 warps x one 32x128 B box
+};
 constexpr int PA_BYTES = 128 * BK / 2;   // this CTA's 128 rows of A
 constexpr int PB_BYTES = 128 * BK / 2;   // this CTA's 128 rows of B
 constexpr int PSFA_BYTES = 2048;         // 4 atoms of this CTA's 128 A rows
 constexpr int PSFB_BYTES = 4096;         // 2 row tiles x 4 atoms: all 256 rows of the B tile
 constexpr int PSTAGE_BYTES = PA_BYTES + PB_BYTES + PSFA_BYTES + PSFB_BYTES;
-constexpr int SMEM_BYTES_PAIR = kStagesPair * PSTAGE_BYTES + 1024 + 1024;
+template <int OUT_BF16>
+constexpr int smem_bytes_pair() {
+  return PairCfg<OUT_BF16>::kStages * PSTAGE_BYTES + PairCfg<OUT_BF16>::kStaging + 1024 + 1024;
+}
 constexpr int kSfWarps = 4;
 constexpr int kSfBufs = 4;  // TMEM scale buffers: 256 + 4 x 48 = 448 columns
 constexpr int kThreadsPair = 64 + 32 * kEpiWarps + 32 * kSfWarps;
@@ -492,13 +505,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_nvfp4_pair(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b,
                     const __grid_constant__ CUtensorMap tmap_sfa,
-                    const __grid_constant__ CUtensorMap tmap_sfb, const GemmParams p, int groups) {
+                    const __grid_constant__ CUtensorMap tmap_sfb,
+                    const __grid_constant__ CUtensorMap tmap_c, const GemmParams p, int groups) {
+  constexpr int kStagesPair = PairCfg<OUT_BF16>::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~(uintptr_t)1023);
   uint8_t* sm_a = smem;
   uint8_t* sm_b = sm_a + kStagesPair * PA_BYTES;
-  uint8_t* sm_sfa = sm_b + kStagesPair * PB_BYTES;
+  uint8_t* sm_stage_out = sm_b + kStagesPair * PB_BYTES;  // 1024-aligned
+  uint8_t* sm_sfa = sm_stage_out + PairCfg<OUT_BF16>::kStaging;
   uint8_t* sm_sfb = sm_sfa + kStagesPair * PSFA_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm_sfb + kStagesPair * PSFB_BYTES);
   uint64_t* empty = full + kStagesPair;
@@ -523,6 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     prefetch_tmap(&tmap_b);
     prefetch_tmap(&tmap_sfa);
     prefetch_tmap(&tmap_sfb);
+    if (OUT_BF16) prefetch_tmap(&tmap_c);
     for (int s = 0; s < kStagesPair; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -679,11 +696,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       const int64_t row = (int64_t)tc.mt * 256 + 128 * rank + 32 * q + lane;
       const int64_t colh = (int64_t)tc.nt * BN + 128 * h;
       if (OUT_BF16) {
-        // each 32-column slice is converted and stored as soon as it is loaded
-        // (stores are fire-and-forget); TMEM is released after the last load
-        __nv_bfloat16* out =
-            reinterpret_cast<__nv_bfloat16*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + colh;
-        const bool vec = colh + 128 <= p.N && (((uintptr_t)out) & 15) == 0;
+        // TMEM -> registers -> bf16 -> this warp's 128-byte-swizzled staging
+        // slice (32 rows x 128 columns = two TMA boxes); release TMEM, then
+        // one elected lane TMA-stores the slice (clipped at M / N).
+        const uint32_t stage = smem_u32(sm_stage_out) + (uint32_t)(warp - 2) * 4096;
+        const uint32_t box = stage + lane * 128;
+        if (lane == 0) bulk_wait_read<0>();  // previous tile's store has read the box
+        __syncwarp();
+        uint32_t keep[2][16];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           uint32_t r[32];
@@ -694,7 +714,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
           }
-          if (row >= p.M) continue;
           uint32_t w[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
@@ -702,16 +721,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                                                      __uint_as_float(r[2 * k + 1]) * alpha);
             w[k] = *reinterpret_cast<uint32_t*>(&v);
           }
-          if (vec) {
+          if (i < 2) {
 #pragma unroll
-            for (int k = 0; k < 16; k += 4)
-              *reinterpret_cast<uint4*>(out + 32 * i + 2 * k) = make_uint4(w[k], w[k + 1], w[k + 2], w[k + 3]);
+            for (int k = 0; k < 4; ++k) {
+              const int j = i * 4 + k;  // 16-byte chunk within the 128-byte row
+              sts128(box + ((j ^ (lane & 7)) << 4), w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+            }
           } else {
-            for (int e = 0; e < 32; ++e)
-              if (colh + 32 * i + e < p.N)
-                reinterpret_cast<uint16_t*>(out)[32 * i + e] = (uint16_t)(w[e >> 1] >> (16 * (e & 1)));
+#pragma unroll
+            for (int k = 0; k < 16; ++k) keep[i - 2][k] = w[k];
           }
         }
+        const int col = tc.nt * BN + 128 * h;
+        const int rowb = tc.mt * 256 + 128 * (int)rank + 32 * q;
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmap_c, stage, col, rowb, tc.g);
+          bulk_commit();
+          bulk_wait_read<0>();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int j = i * 4 + k;
+            sts128(box + ((j ^ (lane & 7)) << 4), keep[i][4 * k], keep[i][4 * k + 1],
+                   keep[i][4 * k + 2], keep[i][4 * k + 3]);
+          }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmap_c, stage, col + 64, rowb, tc.g);
+          bulk_commit();
+        }
+        continue;
       } else {
         // f32: store each 32-column slice as soon as it is loaded, release after the last
         float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + colh;
@@ -741,6 +786,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       }
     }
   }
+  if (OUT_BF16 && warp >= 2 && warp < 2 + kEpiWarps && lane == 0) bulk_wait<0>();
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // no CTA leaves while its peer may still signal its barriers
@@ -801,6 +847,21 @@ bool make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t groups, int64_t grou
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D map over C [groups][M][ldc] (bf16), box 64 columns (128 bytes) x 32
+// rows, 128-byte swizzle: the pair kernel's epilogue staging layout.
+bool make_out_map(CUtensorMap* m, void* c, int64_t groups, int64_t M, int64_t N, int64_t ldc,
+                  int esz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || ((ldc * esz) % 16) != 0 || (((uintptr_t)c) & 15) != 0) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)groups};
+  const cuuint64_t strides[2] = {(cuuint64_t)(ldc * esz), (cuuint64_t)(ldc * esz * M)};
+  const cuuint32_t box[3] = {(cuuint32_t)(128 / esz), 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const double* alpha_a,
                 const uint8_t* b_codes, const uint8_t* b_sf, const double* alpha_b, int64_t M,
                 int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype, int alpha_per_group,
@@ -845,23 +906,26 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   const char* sel = getenv("F46_GEMM_KERNEL");
   const bool want_pair = !getenv("F46_GEMM_SIMPLE") && !getenv("F46_GEMM_1SM") &&
                          !(sel && sel[0] != 'p');
-  CUtensorMap msfa, msfb, mb_half;
-  if (want_pair && make_sf_map(&msfa, a_sf, groups, p.sfa_group_stride) &&
+  CUtensorMap msfa, msfb, mb_half, mc;
+  const bool cmap = p.c_bf16 && make_out_map(&mc, c, groups, M, N, ldc, 2);
+  if (!cmap) memset(&mc, 0, sizeof(mc));
+  // (bf16 into an ldc the TMA store cannot express takes the single-CTA kernel)
+  if (want_pair && (cmap || !p.c_bf16) && make_sf_map(&msfa, a_sf, groups, p.sfa_group_stride) &&
       make_sf_map(&msfb, b_sf, groups, p.sfb_group_stride) &&
       make_code_map(&mb_half, b_codes, groups, N, kbytes, 128)) {
     static std::once_flag pair_once;
     std::call_once(pair_once, [] {
       cudaFuncSetAttribute(gemm_nvfp4_pair<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES_PAIR);
+                           smem_bytes_pair<0>());
       cudaFuncSetAttribute(gemm_nvfp4_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES_PAIR);
+                           smem_bytes_pair<1>());
     });
     const int64_t tiles = (int64_t)groups * ((M + 255) / 256) * ((N + BN - 1) / BN);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(tiles, sms / 2);
-    if (p.c_bf16)
-      gemm_nvfp4_pair<1><<<grid, kThreadsPair, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+    if (cmap)
+      gemm_nvfp4_pair<1><<<grid, kThreadsPair, smem_bytes_pair<1>(), stream>>>(ma, mb_half, msfa, msfb, mc, p, groups);
     else
-      gemm_nvfp4_pair<0><<<grid, kThreadsPair, SMEM_BYTES_PAIR, stream>>>(ma, mb_half, msfa, msfb, p, groups);
+      gemm_nvfp4_pair<0><<<grid, kThreadsPair, smem_bytes_pair<0>(), stream>>>(ma, mb_half, msfa, msfb, mc, p, groups);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
       fprintf(stderr, "[fouroversix] gemm (pair) launch: %s\n", cudaGetErrorString(e));
