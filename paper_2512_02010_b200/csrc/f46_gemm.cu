@@ -480,10 +480,14 @@ __global__ void __launch_bounds__(kThreadsP, 1)
 // ahead of the release stalled it: 221 -> 180 us when compiled out).  Each
 // epilogue warp stages the first 64 of its 128 columns, keeps the other 64
 // packed in registers, releases TMEM, then stores the two boxes in turn.
+// OUT_BF16: 0 = f32 stored directly (any ldc), 1 = bf16 through one staged
+// 32x64 box per warp, 2 = f32 through one staged 32x32 box per warp (chunk 0
+// staged, chunks 1-3 in registers until TMEM is released).  Both staged
+// variants keep five operand stages: four measurably starve the tensor pipe.
 template <int OUT_BF16>
 struct PairCfg {
   static constexpr int kStages = 5;
-  static constexpr int kStaging = OUT_BF16 ? 8 * 4096 : 0;  // 8 warps x one 32x128 B box
+  static constexpr int kStaging = OUT_BF16 == 1 ? 8 * 4096 : (OUT_BF16 == 2 ? 8 * 4096 : 0);
 };
 constexpr int PA_BYTES = 128 * BK / 2;   // this CTA's 128 rows of A
 constexpr int PB_BYTES = 128 * BK / 2;   // this CTA's 128 rows of B
@@ -539,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     prefetch_tmap(&tmap_b);
     prefetch_tmap(&tmap_sfa);
     prefetch_tmap(&tmap_sfb);
-    if (OUT_BF16) prefetch_tmap(&tmap_c);
+    if (OUT_BF16) prefetch_tmap(&tmap_c);  // 1, 2: staged TMA-store epilogues
     for (int s = 0; s < kStagesPair; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -695,7 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #endif
       const int64_t row = (int64_t)tc.mt * 256 + 128 * rank + 32 * q + lane;
       const int64_t colh = (int64_t)tc.nt * BN + 128 * h;
-      if (OUT_BF16) {
+      if (OUT_BF16 == 1) {
         // TMEM -> registers -> bf16 -> this warp's 128-byte-swizzled staging
         // slice (32 rows x 128 columns = two TMA boxes); release TMEM, then
         // one elected lane TMA-stores the slice (clipped at M / N).
@@ -757,6 +761,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           bulk_commit();
         }
         continue;
+      } else if (OUT_BF16 == 2) {
+        // f32: chunk 0 staged in this warp's 32x32 f32 box, chunks 1-3 kept in
+        // registers; release TMEM; then store the box and refill it three times
+        const uint32_t stage = smem_u32(sm_stage_out) + (uint32_t)(warp - 2) * 4096;
+        const uint32_t box = stage + lane * 128;
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint32_t keep[3][32];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[32];
+          tc_ld_32x32b_x32(taddr + 32 * i, r);
+          tc_wait_ld();
+          if (i == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+          }
+#pragma unroll
+          for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
+          if (i == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              sts128(box + ((j ^ (lane & 7)) << 4), r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) keep[i - 1][k] = r[k];
+          }
+        }
+        const int col = tc.nt * BN + 128 * h;
+        const int rowb = tc.mt * 256 + 128 * (int)rank + 32 * q;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i > 0) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              sts128(box + ((j ^ (lane & 7)) << 4), keep[i - 1][4 * j], keep[i - 1][4 * j + 1],
+                     keep[i - 1][4 * j + 2], keep[i - 1][4 * j + 3]);
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmap_c, stage, col + 32 * i, rowb, tc.g);
+            bulk_commit();
+          }
+        }
+        continue;
       } else {
         // f32: store each 32-column slice as soon as it is loaded, release after the last
         float* out = reinterpret_cast<float*>(p.c) + tc.g * p.c_group_stride + row * p.ldc + colh;
@@ -786,7 +839,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
       }
     }
   }
-  if (OUT_BF16 && warp >= 2 && warp < 2 + kEpiWarps && lane == 0) bulk_wait<0>();
+  if (OUT_BF16 != 0 && warp >= 2 && warp < 2 + kEpiWarps && lane == 0) bulk_wait<0>();
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // no CTA leaves while its peer may still signal its barriers
@@ -857,8 +910,8 @@ bool make_out_map(CUtensorMap* m, void* c, int64_t groups, int64_t M, int64_t N,
   const cuuint64_t strides[2] = {(cuuint64_t)(ldc * esz), (cuuint64_t)(ldc * esz * M)};
   const cuuint32_t box[3] = {(cuuint32_t)(128 / esz), 32, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, c, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  return fn(m, esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c,
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -907,7 +960,8 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   const bool want_pair = !getenv("F46_GEMM_SIMPLE") && !getenv("F46_GEMM_1SM") &&
                          !(sel && sel[0] != 'p');
   CUtensorMap msfa, msfb, mb_half, mc;
-  const bool cmap = p.c_bf16 && make_out_map(&mc, c, groups, M, N, ldc, 2);
+  const int esz = p.c_bf16 ? 2 : 4;
+  const bool cmap = make_out_map(&mc, c, groups, M, N, ldc, esz);
   if (!cmap) memset(&mc, 0, sizeof(mc));
   // (bf16 into an ldc the TMA store cannot express takes the single-CTA kernel)
   if (want_pair && (cmap || !p.c_bf16) && make_sf_map(&msfa, a_sf, groups, p.sfa_group_stride) &&
@@ -919,11 +973,15 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
                            smem_bytes_pair<0>());
       cudaFuncSetAttribute(gemm_nvfp4_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem_bytes_pair<1>());
+      cudaFuncSetAttribute(gemm_nvfp4_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_bytes_pair<2>());
     });
     const int64_t tiles = (int64_t)groups * ((M + 255) / 256) * ((N + BN - 1) / BN);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(tiles, sms / 2);
-    if (cmap)
+    if (p.c_bf16)
       gemm_nvfp4_pair<1><<<grid, kThreadsPair, smem_bytes_pair<1>(), stream>>>(ma, mb_half, msfa, msfb, mc, p, groups);
+    else if (cmap)
+      gemm_nvfp4_pair<2><<<grid, kThreadsPair, smem_bytes_pair<2>(), stream>>>(ma, mb_half, msfa, msfb, mc, p, groups);
     else
       gemm_nvfp4_pair<0><<<grid, kThreadsPair, smem_bytes_pair<0>(), stream>>>(ma, mb_half, msfa, msfb, mc, p, groups);
     const cudaError_t e = cudaGetLastError();
