@@ -1328,6 +1328,300 @@ __global__ void __launch_bounds__(256) dequant_vec_kernel(const uint8_t* __restr
   if (nan_scale && d_flags) atomicOr(d_flags, F46_FLAG_NAN_SCALE);
 }
 
+// K3 with TMA-staged stores.  cols % 16 == 0 makes the packed codes and the
+// output one flat stream, so a warp owns a 1024-element chunk: each lane loads
+// 16 contiguous code bytes (two blocks, the warp 512 B coalesced) and their two
+// scale bytes, prefetched one chunk ahead; writes its 32 results into the
+// warp's 128-byte-swizzled staging buffer (bank-conflict free); one lane then
+// stores the chunk with a single cp.async.bulk.tensor (2 or 4 KB) and the warp
+// moves on -- two buffers per warp keep a store in flight while the next chunk
+// is computed.  The output is viewed as [n / EPR rows][128 B]; elements of a
+// ragged last row (n % EPR) are stored directly.  Same arithmetic as
+// dequant_vec_kernel (blockquant.py:363-376).
+template <int OUT>
+struct DqTma {
+  static constexpr int OB = OUT == DT_F32 ? 4 : 2;  // output bytes per element
+  static constexpr int EPR = 128 / OB;               // elements per staged 128-byte row
+  static constexpr int kChunk = 1024;                // elements per warp chunk
+  static constexpr int kBoxRows = kChunk / EPR;
+  static constexpr int kBuf = kChunk * OB;           // bytes per staging buffer
+  static constexpr int kWarpsPerCta = 8;
+  static constexpr int kSmem = kWarpsPerCta * 2 * kBuf;
+#ifndef F46_DQ_U
+#define F46_DQ_U 2
+#endif
+  static constexpr int kU = F46_DQ_U;                  // chunks per warp pass
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_q() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_q() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all_q() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem_q() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts128_q(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+// the scale byte of flat block b
+template <int SL>
+__device__ __forceinline__ uint32_t dq_scale(const uint8_t* __restrict__ scales, int64_t b, int64_t nb,
+                                             int64_t kb4, bool small) {
+  if (SL != F46_SCALES_TC) return __ldg(scales + b);
+  const int64_t row = small ? (int64_t)((uint32_t)b / (uint32_t)nb) : b / nb;
+  return __ldg(scales + sf_tc_offset(row, b - row * nb, kb4));
+}
+
+#ifndef F46_DQ_MINB
+#define F46_DQ_MINB 3
+#endif
+// (vals * alpha) * scale in float64 as blockquant.py:376, one rounding to the
+// output type (bf16: round-to-odd f32 first).  Only for an alpha that is not a
+// float32 (an explicit override); kept out of line so its float64 temporaries do
+// not set the register budget of the common path.
+template <int OUT>
+__device__ __noinline__ float2 dq_f64_pair(float2 vd, double alpha_d) {
+  const double p0 = __dmul_rn((double)vd.x, alpha_d), p1 = __dmul_rn((double)vd.y, alpha_d);
+  if constexpr (OUT == DT_F32) {
+    return make_float2(__double2float_rn(p0), __double2float_rn(p1));
+  } else {
+    const float r0 = __double2float_rz(p0), r1 = __double2float_rz(p1);
+    return make_float2(__uint_as_float(__float_as_uint(r0) | ((double)r0 != p0 ? 1u : 0u)),
+                       __uint_as_float(__float_as_uint(r1) | ((double)r1 != p1 ? 1u : 0u)));
+  }
+}
+
+// Shape constants of one K3 launch, prepared on the host.  The flat block index
+// b -> (row, kb) division uses a multiply-high by a precomputed magic number
+// (round-up method) when every block index fits 32 bits.
+struct DqArgs {
+  int64_t rows, cols, n, nb, kb4;
+  uint32_t magic, sh1, sh2;  // row = (t + ((b - t) >> sh1)) >> sh2, t = umulhi(b, magic)
+  int fast32;                // block indices and scale offsets fit 32 bits
+  int pair16;                // the lane's two scale bytes are adjacent and 2-byte aligned
+};
+
+// The two scale bytes of flat blocks b0, b0 + 1 (b0 even).
+template <int SL>
+__device__ __forceinline__ void dq_scales2(const uint8_t* __restrict__ scales, const DqArgs& a,
+                                           int64_t b0, uint32_t& s0, uint32_t& s1) {
+  if (SL != F46_SCALES_TC) {
+    if (a.pair16) {
+      const uint32_t v = __ldg(reinterpret_cast<const uint16_t*>(scales + b0));
+      s0 = v & 0xFF;
+      s1 = v >> 8;
+    } else {
+      s0 = __ldg(scales + b0);
+      s1 = __ldg(scales + b0 + 1);
+    }
+    return;
+  }
+  if (a.fast32) {
+    const uint32_t b = (uint32_t)b0, t = __umulhi(b, a.magic);
+    const uint32_t r = (t + ((b - t) >> a.sh1)) >> a.sh2;
+    const uint32_t kb = b - r * (uint32_t)a.nb;
+    const uint32_t off = ((r >> 7) * (uint32_t)a.kb4 + (kb >> 2)) * 512 + (r & 31) * 16 +
+                         ((r & 127) >> 5) * 4 + (kb & 3);
+    if (a.pair16) {  // nb even: b0, b0 + 1 share the row and the 4-byte scale group
+      const uint32_t v = __ldg(reinterpret_cast<const uint16_t*>(scales + off));
+      s0 = v & 0xFF;
+      s1 = v >> 8;
+      return;
+    }
+    s0 = __ldg(scales + off);
+  } else {
+    s0 = dq_scale<SL>(scales, b0, a.nb, a.kb4, false);
+  }
+  s1 = dq_scale<SL>(scales, b0 + 1, a.nb, a.kb4, false);
+}
+
+// Alpha handling of one K3 launch, decided once per CTA from the device alpha:
+//  DQ_DIRECT  f32 alpha and one f32 rounding is the answer: f32 output always;
+//             bf16 output when no value can double-round (dq_bf16_direct_ok)
+//  DQ_ODD     f32 alpha, bf16 output through a round-to-odd f32 product
+//  DQ_F64     alpha not a float32 (explicit override): float64 product
+enum { DQ_DIRECT = 0, DQ_ODD = 1, DQ_F64 = 2 };
+
+// bf16(RN32(p * alpha)) == RN_bf16(p * alpha) for every decoded value p =
+// fp4 * scale when RN32 never lands on a bf16 midpoint from off it.  p has at
+// most 6 significant bits (2 from the FP4 value, 4 from the E4M3 scale), so
+// p = m * 2^k with m odd <= 45 < 64, and while p * alpha stays a normal float
+// the property of m * alpha decides it for every k.  One lane per odd m.
+__device__ __forceinline__ bool dq_bf16_direct_ok(float alpha) {
+  const int lane = threadIdx.x & 31;
+  const float m = (float)(2 * lane + 1);
+  const float y = __fmul_rn(m, alpha);
+  const bool bad = (__float_as_uint(y) & 0xFFFFu) == 0x8000u && (double)y != (double)m * (double)alpha;
+  // smallest nonzero |p| is 0.5 * 2^-9; largest 6 * 448
+  const bool range = alpha >= 0x1p-115f && alpha <= 0x1p+114f;
+  return !__any_sync(0xFFFFFFFFu, bad) && range;
+}
+
+template <int OUT, int SL, int AM>
+__device__ __forceinline__ void dq_tma_body(const CUtensorMap* tmap_out, const uint8_t* __restrict__ codes,
+                                            const uint8_t* __restrict__ scales, double alpha_d,
+                                            const DqArgs& a, void* out, uint32_t* d_flags) {
+  using C = DqTma<OUT>;
+  extern __shared__ __align__(1024) uint8_t dq_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = a.n;
+  const int64_t nch = (n + C::kChunk - 1) / C::kChunk;
+  const int64_t ntma = (n / C::EPR) * C::EPR;  // elements the tensor map covers
+  const float alpha = (float)alpha_d;
+  const float2 a2 = make_float2(alpha, alpha);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(dq_smem) + (uint32_t)warp * 2 * C::kBuf;
+  const int64_t G = (int64_t)gridDim.x * C::kWarpsPerCta;
+  bool nan_scale = false;
+
+  // lane's 32 codes (two blocks) and their two scale bytes for chunk ch
+  auto load = [&](int64_t ch, uint4& cw, uint32_t& s0, uint32_t& s1) {
+    const int64_t e0 = ch * C::kChunk + lane * 32;
+    cw = make_uint4(0, 0, 0, 0);
+    s0 = s1 = 0x38;  // 1.0: harmless for padding lanes
+    if (e0 + 32 <= n) {
+      cw = __ldg(reinterpret_cast<const uint4*>(codes + (e0 >> 1)));
+      dq_scales2<SL>(scales, a, e0 >> 4, s0, s1);
+    } else if (e0 < n) {  // n % 16 == 0: exactly one valid block
+      const uint2 h = __ldg(reinterpret_cast<const uint2*>(codes + (e0 >> 1)));
+      cw.x = h.x;
+      cw.y = h.y;
+      s0 = dq_scale<SL>(scales, e0 >> 4, a.nb, a.kb4, false);
+    }
+  };
+
+  // a warp takes kU consecutive chunks per pass, all their loads in flight first
+  constexpr int kU = C::kU;
+  const int64_t nsup = (nch + kU - 1) / kU;
+  int it = 0;
+  for (int64_t sup = blockIdx.x * (int64_t)C::kWarpsPerCta + warp; sup < nsup; sup += G) {
+    uint4 cwv[kU];
+    uint32_t s0v[kU], s1v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) load(sup * kU + u, cwv[u], s0v[u], s1v[u]);
+#pragma unroll 1
+    for (int u = 0; u < kU; ++u, ++it) {
+      const int64_t ch = sup * kU + u;
+      if (ch >= nch) break;
+      // always consume slot 0, then rotate (keeps the body compiled once without
+      // dynamically indexing the register arrays)
+      const uint4 cw = cwv[0];
+      const uint32_t s0 = s0v[0], s1 = s1v[0];
+#pragma unroll
+      for (int v = 0; v + 1 < kU; ++v) {
+        cwv[v] = cwv[v + 1];
+        s0v[v] = s0v[v + 1];
+        s1v[v] = s1v[v + 1];
+      }
+      const int64_t e0 = ch * C::kChunk + lane * 32;
+      const bool valid0 = e0 < n, valid1 = e0 + 16 < n;
+      nan_scale |= (valid0 && (s0 & 0x7F) == 0x7F) || (valid1 && (s1 & 0x7F) == 0x7F);
+      uint32_t o[32 * C::OB / 4];  // the lane's output bytes as words
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk) {
+        const uint32_t sc = blk ? s1 : s0;
+        const float delta = e4m3_to_f32(sc & 0x7F) * ((sc & 0x80) ? -1.f : 1.f);
+        const float2 d2 = make_float2(delta, delta);
+#pragma unroll
+        for (int wi = 0; wi < 2; ++wi) {
+          const uint32_t w = blk ? (wi ? cw.w : cw.z) : (wi ? cw.y : cw.x);
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            uint32_t h;
+            switch (pp) {
+              case 0: { const __half2 q = e2m1x2_to_h2<0>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+              case 1: { const __half2 q = e2m1x2_to_h2<1>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+              case 2: { const __half2 q = e2m1x2_to_h2<2>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+              default: { const __half2 q = e2m1x2_to_h2<3>(w); h = *reinterpret_cast<const uint32_t*>(&q); } break;
+            }
+            const float2 vd = __fmul2_rn(make_float2(fhadd_h<0>(h, -0.f), fhadd_h<1>(h, -0.f)), d2);
+            float y0, y1;
+            if constexpr (AM == DQ_F64) {
+              const float2 r = dq_f64_pair<OUT>(vd, alpha_d);
+              y0 = r.x;
+              y1 = r.y;
+            } else if constexpr (AM == DQ_DIRECT) {
+              const float2 r = __fmul2_rn(vd, a2);
+              y0 = r.x;
+              y1 = r.y;
+            } else {
+              // round-to-odd to f32, then RN to bf16 == one rounding of the exact product
+              const float r0 = __fmul_rz(vd.x, alpha), r1 = __fmul_rz(vd.y, alpha);
+              y0 = __uint_as_float(__float_as_uint(r0) | (fmaf(vd.x, alpha, -r0) != 0.f ? 1u : 0u));
+              y1 = __uint_as_float(__float_as_uint(r1) | (fmaf(vd.y, alpha, -r1) != 0.f ? 1u : 0u));
+            }
+            const int e = blk * 16 + wi * 8 + pp * 2;  // element index within the lane's 32
+            if constexpr (OUT == DT_F32) {
+              o[e] = __float_as_uint(y0);
+              o[e + 1] = __float_as_uint(y1);
+            } else {
+              const __nv_bfloat162 hb = __floats2bfloat162_rn(y0, y1);
+              o[e >> 1] = *reinterpret_cast<const uint32_t*>(&hb);
+            }
+          }
+        }
+      }
+      // staging buffer `it & 1` was last read by the store committed two chunks ago
+      const uint32_t buf = sbase + (uint32_t)(it & 1) * C::kBuf;
+      if (lane == 0) bulk_wait_read_q<1>();
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 32 * C::OB / 16; ++c) {
+        // 16-byte chunk c of the lane's bytes -> staged row r, logical chunk lc
+        const int r = OUT == DT_F32 ? lane : (lane >> 1);
+        const int lc = OUT == DT_F32 ? c : ((lane & 1) * 4 + c);
+        sts128_q(buf + r * 128 + ((lc ^ (r & 7)) << 4), o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+      }
+      fence_async_smem_q();
+      __syncwarp();
+      if (lane == 0 && ch * C::kChunk < ntma) {
+        tma_store_2d(tmap_out, buf, 0, (int)(ch * C::kBoxRows));
+        bulk_commit_q();
+      }
+      // elements past the tensor map (a ragged last 128-byte row) go out directly
+      if (e0 + 32 > ntma && e0 < n) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int64_t e = e0 + i;
+          if (e >= ntma && e < n) {
+            if constexpr (OUT == DT_F32)
+              reinterpret_cast<uint32_t*>(out)[e] = o[i];
+            else
+              reinterpret_cast<uint16_t*>(out)[e] = (uint16_t)(o[i >> 1] >> (16 * (i & 1)));
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0) bulk_wait_all_q();
+  if (nan_scale && d_flags) atomicOr(d_flags, F46_FLAG_NAN_SCALE);
+}
+
+template <int OUT, int SL>
+__global__ void __launch_bounds__(256, F46_DQ_MINB) dequant_tma_kernel(const __grid_constant__ CUtensorMap tmap_out,
+                                                          const uint8_t* __restrict__ codes,
+                                                          const uint8_t* __restrict__ scales,
+                                                          const double* d_alpha, const DqArgs a,
+                                                          void* out, uint32_t* d_flags) {
+  const double alpha_d = *d_alpha;
+  if ((double)(float)alpha_d != alpha_d) {
+    dq_tma_body<OUT, SL, DQ_F64>(&tmap_out, codes, scales, alpha_d, a, out, d_flags);
+  } else if (OUT == DT_F32 || dq_bf16_direct_ok((float)alpha_d)) {
+    dq_tma_body<OUT, SL, DQ_DIRECT>(&tmap_out, codes, scales, alpha_d, a, out, d_flags);
+  } else {
+    dq_tma_body<OUT, SL, (OUT == DT_F32 ? DQ_DIRECT : DQ_ODD)>(&tmap_out, codes, scales, alpha_d, a, out,
+                                                               d_flags);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Host helpers
 // ---------------------------------------------------------------------------
@@ -1410,6 +1704,74 @@ int dispatch_mode(const QParams& p, cudaStream_t s, bool tma) {
     default:
       return launch_quant<DT, ADAPTIVE>(p, s, tma);
   }
+}
+
+template <int OUT, int SL>
+int launch_dequant_tma_t(const CUtensorMap& map, const uint8_t* codes, const uint8_t* scales,
+                         const double* d_alpha, const DqArgs& a, void* out, uint32_t* d_flags,
+                         cudaStream_t s) {
+  using C = DqTma<OUT>;
+  static int ctas_per_sm = 0;
+  if (ctas_per_sm == 0) {
+    cudaFuncSetAttribute(dequant_tma_kernel<OUT, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, dequant_tma_kernel<OUT, SL>,
+                                                  C::kWarpsPerCta * 32, C::kSmem);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+  }
+  const int64_t nsup = (a.n + (int64_t)C::kChunk * C::kU - 1) / ((int64_t)C::kChunk * C::kU);
+  int64_t grid = (nsup + C::kWarpsPerCta - 1) / C::kWarpsPerCta;
+  const int64_t cap = (int64_t)num_sms() * ctas_per_sm;
+  if (grid > cap) grid = cap;
+  dequant_tma_kernel<OUT, SL><<<(unsigned)grid, C::kWarpsPerCta * 32, C::kSmem, s>>>(
+      map, codes, scales, d_alpha, a, out, d_flags);
+  return launch_status();
+}
+
+// Unsigned 32-bit division by d via multiply-high (round-up method):
+// q = (t + ((x - t) >> sh1)) >> sh2 with t = umulhi(x, magic), exact for all x < 2^32.
+void udiv_magic(uint32_t d, uint32_t* magic, uint32_t* sh1, uint32_t* sh2) {
+  int l = 0;
+  while (l < 32 && (1ull << l) < d) ++l;  // l = ceil(log2 d)
+  *magic = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+  *sh1 = l < 1 ? l : 1;
+  *sh2 = l > 1 ? l - 1 : 0;
+}
+
+// F46_ERR_UNSUPPORTED when the output cannot be described by a tensor map
+int launch_dequant_tma(const uint8_t* codes, const uint8_t* scales, bool tc, const double* d_alpha,
+                       int64_t rows, int64_t cols, void* out, int out_dtype, uint32_t* d_flags,
+                       cudaStream_t s) {
+  EncodeTiledFn fn = get_encode_fn();
+  const bool f32 = out_dtype == F46_DT_F32;
+  const int epr = f32 ? DqTma<DT_F32>::EPR : DqTma<DT_BF16>::EPR;
+  const int box_rows = f32 ? DqTma<DT_F32>::kBoxRows : DqTma<DT_BF16>::kBoxRows;
+  const int64_t trows = rows * cols / epr;
+  if (!fn || trows < 1 || trows > 0x7FFFFFFFll) return F46_ERR_UNSUPPORTED;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)epr, (cuuint64_t)trows};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {(cuuint32_t)epr, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  if (fn(&map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out,
+         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return F46_ERR_UNSUPPORTED;
+  DqArgs a;
+  a.rows = rows;
+  a.cols = cols;
+  a.n = rows * cols;
+  a.nb = cols >> 4;
+  a.kb4 = (a.nb + 3) >> 2;
+  udiv_magic((uint32_t)std::min<int64_t>(a.nb, 0xFFFFFFFFll), &a.magic, &a.sh1, &a.sh2);
+  const int64_t sf_bytes = ((rows + 127) / 128) * a.kb4 * 512;
+  a.fast32 = rows * a.nb < (1ll << 32) && sf_bytes < (1ll << 32) && a.nb < (1ll << 32);
+  a.pair16 = (((uintptr_t)scales) & 1) == 0 && (!tc || a.nb % 2 == 0);
+  if (f32)
+    return tc ? launch_dequant_tma_t<DT_F32, F46_SCALES_TC>(map, codes, scales, d_alpha, a, out, d_flags, s)
+              : launch_dequant_tma_t<DT_F32, F46_SCALES_RM>(map, codes, scales, d_alpha, a, out, d_flags, s);
+  return tc ? launch_dequant_tma_t<DT_BF16, F46_SCALES_TC>(map, codes, scales, d_alpha, a, out, d_flags, s)
+            : launch_dequant_tma_t<DT_BF16, F46_SCALES_RM>(map, codes, scales, d_alpha, a, out, d_flags, s);
 }
 
 }  // namespace
@@ -1499,6 +1861,12 @@ int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
   const bool tc = scale_layout == F46_SCALES_TC;
+  // TMA-staged path: f32 / bf16 out, cols % 16 == 0, 16-byte aligned codes and output
+  if ((out_dtype == F46_DT_F32 || out_dtype == F46_DT_BF16) && cols % 16 == 0 &&
+      (((uintptr_t)out) & 15) == 0 && (((uintptr_t)codes) & 15) == 0 && !getenv("F46_DQ_VEC")) {
+    const int rc = launch_dequant_tma(codes, scales, tc, d_alpha, rows, cols, out, out_dtype, d_flags, s);
+    if (rc != F46_ERR_UNSUPPORTED) return rc;
+  }
   // coalesced path: f32 / bf16 out, cols % 16 == 0, 16-byte aligned rows
   if ((out_dtype == F46_DT_F32 || out_dtype == F46_DT_BF16) && cols % 16 == 0 &&
       (((uintptr_t)out) & 15) == 0 && (((uintptr_t)codes) & 3) == 0) {

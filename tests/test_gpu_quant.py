@@ -170,3 +170,25 @@ def test_reference_style_float64_inputs():
     assert np.array_equal(q.packed_codes.cpu().numpy(), ref["codes"])
     D = f46.dequantize_tensor(q, torch.float64).cpu().numpy()
     assert np.array_equal(D, O.dequantize(ref["codes"], ref["scales"], ref["alpha"], 8, 48))
+
+
+# 0.008766868151724339 is a float32 for which RN32(11 * alpha) is an inexact bf16
+# midpoint: bf16 output must take the round-to-odd route (DQ_ODD)
+@pytest.mark.parametrize("alpha", [None, 0.003, 0.008766868151724339])
+@pytest.mark.parametrize("shape", [(5, 48), (1, 16), (3, 1040), (33, 4112), (64, 1024), (257, 2064),
+                                   (130, 272)])
+@pytest.mark.parametrize("path", ["tma", "vec"])
+def test_dequant_flat_paths_ragged(shape, alpha, path, monkeypatch):
+    """K3's TMA-staged and coalesced variants on chunk- and row-ragged shapes
+    (odd blocks per row too), with f32-exact alphas (direct and round-to-odd
+    bf16 routes) and an f64-only alpha: f32 is the exact value rounded once,
+    bf16 likewise (a single rounding of the float64 value)."""
+    if path == "vec":
+        monkeypatch.setenv("F46_DQ_VEC", "1")
+    x = bf16_randn(shape, shape[0] * 31 + shape[1])
+    q = run(x.cuda(), "adaptive", alpha=alpha)
+    d64 = f46.dequantize_tensor(q, torch.float64).cpu().numpy()
+    d32 = f46.dequantize_tensor(q, torch.float32).cpu().numpy()
+    assert np.array_equal(d32, d64.astype(np.float32))
+    d16 = f46.dequantize_tensor(q, torch.bfloat16).cpu().view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(d16, f64_to_bf16_bits(d64))

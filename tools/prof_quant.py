@@ -27,7 +27,7 @@ for i in range(int(os.environ.get("ITERS", 3))):
                    codes.data_ptr(), scales.data_ptr(), None, None, None, None, s)
     if os.environ.get("DEQ"):
         out = torch.empty((rows, cols), dtype=torch.bfloat16, device=dev)
-        alpha = torch.tensor([0.003], dtype=torch.float64, device=dev)
+        alpha = torch.tensor([float(torch.tensor(0.003, dtype=torch.float32))], dtype=torch.float64, device=dev)  # f32-exact, as quantize writes it
         L.f46_dequantize(codes.data_ptr(), scales.data_ptr(), 0, alpha.data_ptr(), rows, cols,
                          out.data_ptr(), _lib.DT_BF16, None, s)
 torch.cuda.synchronize()
