@@ -267,6 +267,83 @@ __device__ __forceinline__ void exact_block_global(ExactArgs a, double alpha, ui
   if (a.pick4) a.pick4[row * nb + kbg] = (uint8_t)o.pick4;
 }
 
+// A block the streaming loop deferred (cols % 16 == 0, not force_exact).  Most
+// deferrals are a near-tie block scale or a 4/6 decision inside the f32
+// tolerance, not a value outside the fast path's range, so the exact answer is
+// reached without the float64 quantizer: both scale codes are settled exactly
+// (block_scale_code's tie test), both candidates' codes come from the proven
+// bracket logic (exact_codes), and only the two error sums are recomputed in
+// float64 in the reference's pairwise order (exact_sq_sum) -- the reference's
+// own arithmetic on identical codes (blockquant.py:279, :289-290; adaptive.py:
+// 77-80).  Zero, out-of-range and underflowing blocks take exact_block_global.
+template <int DT, int MODE>
+__device__ __noinline__ void resolve_block_global(ExactArgs a, TensorConsts tc, uint32_t blk,
+                                                  uint32_t kb4, uint32_t* flags) {
+  const uint32_t nb = (uint32_t)(a.cols >> 4);
+  const uint32_t row = blk / nb, kbg = blk - row * nb;
+  const int64_t e0 = (int64_t)row * a.cols + (int64_t)kbg * 16;
+  auto load = [&](int i) -> float {
+    if constexpr (DT == DT_BF16)
+      return __uint_as_float((uint32_t)(reinterpret_cast<const uint16_t*>(a.x)[e0 + i]) << 16);
+    else
+      return reinterpret_cast<const float*>(a.x)[e0 + i];
+  };
+  float2 x[8];
+  float bmax = 0.f;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    x[p] = make_float2(load(2 * p), load(2 * p + 1));
+    bmax = fmax_nan(bmax, fmax_nan(fabsf(x[p].x), fabsf(x[p].y)));
+  }
+  const uint32_t bb = __float_as_uint(bmax);
+  if ((bb - 0x2B800000u) >= 0x28000000u) {  // zero, tiny, huge or non-finite
+    exact_block_global<DT>(a, tc.alpha_d, blk, kb4, flags);
+    return;
+  }
+  const float alpha = tc.alpha;
+  BlockOut o;
+  if constexpr (MODE == FIXED6 || MODE == FIXED4) {
+    const float m = MODE == FIXED6 ? 6.f : 4.f;
+    const uint32_t sc = block_scale_code(bmax, alpha, m, MODE == FIXED6 ? tc.r6_lo : tc.r4_lo,
+                                         MODE == FIXED6 ? tc.r6_hi : tc.r4_hi);
+    if (sc == 0) {
+      exact_block_global<DT>(a, tc.alpha_d, blk, kb4, flags);
+      return;
+    }
+    const float delta = e4m3_to_f32(sc);
+    const float rq = rcp_approx(alpha * delta) * F46_QLO;
+    o.codes = exact_codes(x, rq, alpha, delta, tc.tdir, load);
+    o.sc = sc;
+    o.pick4 = (MODE == FIXED4);
+  } else {
+    const uint32_t sc6 = block_scale_code(bmax, alpha, 6.f, tc.r6_lo, tc.r6_hi);
+    const uint32_t sc4 = block_scale_code(bmax, alpha, 4.f, tc.r4_lo, tc.r4_hi);
+    if (sc6 == 0 || sc4 == 0) {
+      exact_block_global<DT>(a, tc.alpha_d, blk, kb4, flags);
+      return;
+    }
+    const float d6 = e4m3_to_f32(sc6), d4 = e4m3_to_f32(sc4);
+    const uint64_t c6 = exact_codes(x, rcp_approx(alpha * d6) * F46_QLO, alpha, d6, tc.tdir, load);
+    const uint64_t c4 = exact_codes(x, rcp_approx(alpha * d4) * F46_QLO, alpha, d4, tc.tdir, load);
+    double xd[16];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      xd[2 * p] = (double)x[p].x;
+      xd[2 * p + 1] = (double)x[p].y;
+    }
+    const double s6 = exact_sq_sum(xd, c6, tc.alpha_d, (double)d6);
+    const double s4 = exact_sq_sum(xd, c4, tc.alpha_d, (double)d4);
+    const bool k = s4 < s6;  // strict: ties keep 6 (adaptive.py:77-80)
+    o.codes = k ? c4 : c6;
+    o.sc = k ? sc4 : sc6;
+    o.pick4 = k;
+  }
+  *reinterpret_cast<uint64_t*>(a.codes + (int64_t)blk * 8) = o.codes;
+  a.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
+  if (a.scales_rm) a.scales_rm[blk] = (uint8_t)o.sc;
+  if (a.pick4) a.pick4[blk] = (uint8_t)o.pick4;
+}
+
 constexpr int kBPL = kSegElems / 512;   // blocks per lane per segment
 constexpr int kDefer = 2 * kSegElems / 16;  // deferred-block slots per warp (a segment defers <= half)
 
@@ -375,8 +452,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
     __syncwarp();
     if (ndefer) {
       const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
-      const double a = resolve_alpha(p);
-      for (uint32_t i = lane; i < ndefer; i += 32) exact_block_global<DT>(ea, a, dl[i], kb4, p.d_flags);
+      for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
     }
     __syncwarp();
     ndefer = 0;
