@@ -31,6 +31,13 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#ifndef F46_ACC2
+#define F46_ACC2 0
+#endif
+#ifndef F46_PRMT_LO
+#define F46_PRMT_LO 0
+#endif
+
 namespace f46 {
 
 enum { DT_F32 = 0, DT_BF16 = 1, DT_F64 = 2 };
@@ -421,7 +428,11 @@ __device__ __forceinline__ float2 bf16x2_unpack(uint32_t w) {
   asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, h, %2;\n\t}"
       : "=f"(hi)
       : "r"(w), "f"(-0.0f));
+#if F46_PRMT_LO
+  return make_float2(__uint_as_float(__byte_perm(w, 0u, 0x1044u)), hi);
+#else
   return make_float2(__uint_as_float(w << 16), hi);
+#endif
 }
 
 // Quotient-space squared error of one candidate,  sum_i (v_i - q_i)^2  with
@@ -430,6 +441,17 @@ __device__ __forceinline__ float2 bf16x2_unpack(uint32_t w) {
 // relative bound the decision tolerance allows for.
 __device__ __forceinline__ float cand_err(const float2 (&x)[8], float rq) {
   const float2 r2 = make_float2(rq, rq);
+#if F46_ACC2
+  float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const float2 q = __fmul2_rn(x[p], r2);
+    const uint32_t v = e2m1x2_roundtrip(q.y, q.x);
+    const float2 r = make_float2(fhadd_h<0>(v, -q.x), fhadd_h<1>(v, -q.y));
+    acc[p & 1] = __ffma2_rn(r, r, acc[p & 1]);
+  }
+  return (acc[0].x + acc[1].x) + (acc[0].y + acc[1].y);
+#else
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
@@ -439,6 +461,7 @@ __device__ __forceinline__ float cand_err(const float2 (&x)[8], float rq) {
     acc = __ffma2_rn(r, r, acc);
   }
   return acc.x + acc.y;
+#endif
 }
 
 // Packed codes of x * r (16 nibbles, element i at bits [4i, 4i+4)).

@@ -1,17 +1,23 @@
 // f46_quant.cu -- amax, 4/6 quantize and dequantize kernels + their C ABI.
 //
 // Kernels (sm_100a):
-//   amax_kernel        K1: grid-stride 128-bit loads, warp-shuffle max, one
-//                      64-bit atomicMax on the float64 bit pattern per CTA.
-//   quant_tma_kernel   K2: persistent CTAs stream 128-row x 64-col tiles of the
-//                      input through a 3-stage TMA (cp.async.bulk.tensor, 128B
-//                      swizzle) -> shared memory pipeline; one thread owns one
-//                      row of the tile (4 blocks of 16), computes both 4/6
-//                      candidates (f46_device.cuh) and writes 32 B of packed
-//                      E2M1 codes plus 4 E4M3 scales straight into the tcgen05
-//                      128x4 scale layout.  Requires cols % 64 == 0.
-//   quant_generic_kernel  any shape / float64 input: one thread per block.
-//   dequant_kernel     K3: one thread per block, 128-bit stores.
+//   amax_kernel          K1: grid-stride 128-bit loads (4 in flight), warp-shuffle
+//                        max, one 64-bit atomicMax on the float64 bit pattern per CTA.
+//   quant_seg_kernel     K2: each warp streams contiguous 2048-element segments of
+//                        the input through a 2-stage cp.async.bulk -> shared memory
+//                        pipeline; lane l quantizes blocks l, l+32, ... of the
+//                        segment with the straight-line fast path (f46_device.cuh),
+//                        stores 8 B of packed E2M1 codes (coalesced) and the E4M3
+//                        scale into the tcgen05 128x4 layout; uncertified blocks are
+//                        queued per warp and resolved exactly afterwards.
+//                        Requires cols % 16 == 0.
+//   quant_generic_kernel any shape / float64 input: one thread per block.
+//   quant2d_kernel       16x16-tile weight quantization (exact f64), writes W and W^T.
+//   quant_sr_kernel      stochastic rounding with numpy-Philox-exact uniforms.
+//   stats_kernel         fused selection statistics (fraction_4 per rule).
+//   rht16_kernel         16-wide randomized Hadamard transform (f64, numpy order).
+//   dequant_tma_kernel   K3: per-warp 1024-element chunks, TMA-staged stores.
+//   dequant_vec_kernel / dequant_kernel  K3 fallbacks (unaligned / ragged / f64 out).
 //
 // Reference: blockquant.py:215-222, :334-376; adaptive.py:60-101.
 #include <cuda.h>
@@ -29,7 +35,7 @@ using namespace f46;
 namespace {
 
 #ifndef F46_STAGES
-#define F46_STAGES 3
+#define F46_STAGES 2
 #endif
 constexpr int kStages = F46_STAGES;
 
