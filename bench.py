@@ -462,6 +462,35 @@ def bench_gemm(args, dev, peaks):
     e.record(stream)
     torch.cuda.synchronize()
     full_ms = s.elapsed_time(e) / 5
+
+    # producer-fused amax: GEMM -> quantize(C) for the
+    # next layer, with K1 over C (unfused) vs the amax from the GEMM epilogue
+    c16 = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    amax_buf = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def unfused():
+        f46.gemm_nvfp4(aq, bq, torch.bfloat16, out=c16)
+        return f46.quantize_tensor_adaptive(c16, cfg, check_finite=False)
+
+    def fused():
+        f46.gemm_nvfp4(aq, bq, torch.bfloat16, out=c16, amax_out=amax_buf)
+        return f46.quantize_tensor_adaptive(c16, cfg, check_finite=False, d_amax=amax_buf)
+
+    chain = {}
+    for name, fn in (("unfused_ms", unfused), ("fused_ms", fused)):
+        for _ in range(2):
+            fn()
+        s, e = _events(2)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(1_000_000)
+        s.record(stream)
+        for _ in range(5):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize()
+        chain[name] = s.elapsed_time(e) / 5
+    chain["note"] = ("GEMM 8192^3 (bf16 out) + 4/6 quantize of C for the next layer; fused = amax "
+                     "from the GEMM epilogue, so the quantize reads C once")
     return {
         "metric": "4/6-NVFP4 GEMM TFLOP/s", "shape": [M, N, K], "value": tf, "unit": "TFLOP/s",
         "out": out,
@@ -473,6 +502,7 @@ def bench_gemm(args, dev, peaks):
                      "algorithmic_flops_per_launch": flops, "launch_ms": out["bf16"]["ms"],
                      "traffic": profile_traffic("gemm_nvfp4_pair")},
         "quantize_a_b_plus_gemm_ms": full_ms,
+        "gemm_then_quantize_c": chain,
         "data": "synthetic N(0,1) bf16 operands, both quantized with 4/6 (adaptive)",
     }
 

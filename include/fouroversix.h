@@ -162,6 +162,27 @@ int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_
                            f46_stream_t stream);
 
 /*
+ * Producer-fused amax (no reference counterpart --
+ * PAPER.md:153-161's recipe).  As f46_gemm_nvfp4 / f46_gemm_nvfp4_grouped,
+ * and the epilogue also reduces max |C| of the stored values (after the bf16
+ * rounding when c_dtype is bf16) into d_amax_out[0] (grouped: d_amax_out[g]
+ * per group) as a float64, with the same 64-bit atomicMax on the bit pattern
+ * f46_amax uses: the caller zeroes d_amax_out first, and the buffer can be
+ * handed to f46_quantize as its d_amax, so quantizing C for the next layer
+ * reads C once (2.5625 instead of 4.5625 bytes per bf16 element).  A NaN in C
+ * propagates and makes the quantizer flag the input as non-finite.
+ */
+int f46_gemm_nvfp4_amax(const uint8_t* a_codes, const uint8_t* a_scales_tc, const double* d_alpha_a,
+                        const uint8_t* b_codes, const uint8_t* b_scales_tc, const double* d_alpha_b,
+                        int64_t M, int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                        double* d_amax_out, f46_stream_t stream);
+int f46_gemm_nvfp4_grouped_amax(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
+                                const double* d_alpha_a, const uint8_t* b_codes,
+                                const uint8_t* b_scales_tc, const double* d_alpha_b, int64_t M,
+                                int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                                double* d_amax_out, f46_stream_t stream);
+
+/*
  * Selection statistics of the 4/6 rules in one pass (adaptive.py:159-187):
  * for every block both candidates' exact float64 errors and each rule's
  * pick (mse / l1 / absmax, strict '<').  Writes d_partials[nparts][9] =

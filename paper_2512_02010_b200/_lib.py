@@ -39,6 +39,8 @@ EXPORTS = (
     "f46_dequantize",
     "f46_gemm_nvfp4",
     "f46_gemm_nvfp4_grouped",
+    "f46_gemm_nvfp4_amax",
+    "f46_gemm_nvfp4_grouped_amax",
     "f46_selection_stats",
     "f46_quantize_sr",
     "f46_rht16",
@@ -68,6 +70,10 @@ def _declare(L):
     L.f46_gemm_nvfp4.restype = i
     L.f46_gemm_nvfp4_grouped.argtypes = [i, p, p, p, p, p, p, i64, i64, i64, p, i64, i, p]
     L.f46_gemm_nvfp4_grouped.restype = i
+    L.f46_gemm_nvfp4_amax.argtypes = [p, p, p, p, p, p, i64, i64, i64, p, i64, i, p, p]
+    L.f46_gemm_nvfp4_amax.restype = i
+    L.f46_gemm_nvfp4_grouped_amax.argtypes = [i, p, p, p, p, p, p, i64, i64, i64, p, i64, i, p, p]
+    L.f46_gemm_nvfp4_grouped_amax.restype = i
     L.f46_selection_stats.argtypes = [p, i, i64, i64, d, p, d, p, i, p, p]
     L.f46_selection_stats.restype = i
     u64 = ctypes.c_uint64

@@ -72,7 +72,37 @@ struct GemmParams {
   int64_t c_group_stride;                      // elements
   int alpha_group_stride;                      // 0: shared alpha, 1: one per group
   int c_bf16;
+  // Producer-fused amax (nullable): max |C| of each group as the float64 bit
+  // pattern the quantizer's K1 writes (64-bit atomicMax; caller zeroes it), so
+  // the next layer's 4/6 quantize of C skips its amax pass.
+  double* amax_out;
 };
+
+// max(m, |r[0..31]|), NaN-propagating (three-input max, abs folded in)
+__device__ __forceinline__ float absmax32(const uint32_t (&r)[32], float m) {
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(m) : "f"(m), "f"(fabsf(__uint_as_float(r[k]))));
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(m) : "f"(m), "f"(fabsf(__uint_as_float(r[k + 1]))));
+  }
+  return m;
+}
+
+// Stored-value amax of one warp's share of a tile: the largest |acc| scaled by
+// alpha and rounded like the stored element (rounding is monotonic), reduced
+// over the warp, one atomicMax per warp.
+__device__ __forceinline__ void amax_flush(double* dst, float acc_max, float alpha, bool bf16) {
+  float v = acc_max * alpha;
+  if (bf16) v = __bfloat162float(__float2bfloat16_rn(v));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(v), "f"(w));
+  }
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(dst),
+              (unsigned long long)__double_as_longlong((double)v));
+}
 
 template <int OUT_BF16>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -180,10 +210,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 p.alpha_b[g * p.alpha_group_stride]);
     const int64_t row = m0 + 32 * q + lane;
     const bool row_ok = row < p.M;
+    float amx = 0.f;
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t r[32];
       tc_ld_32x32b_x32(tmem + ((uint32_t)(32 * q) << 16) + 32 * c, r);
       tc_wait_ld();
+      if (p.amax_out) amx = absmax32(r, amx);  // padding rows / columns hold zeros
       const int64_t col0 = n0 + 32 * c;
       if (!row_ok || col0 >= p.N) continue;
       if (OUT_BF16) {
@@ -225,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (p.amax_out) amax_flush(p.amax_out + g * p.alpha_group_stride, amx, alpha, OUT_BF16);
   }
   tc_fence_before();
   __syncthreads();
@@ -407,6 +440,12 @@ __global__ void __launch_bounds__(kThreadsP, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty);
+      if (p.amax_out) {
+        float amx = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) amx = absmax32(r[i], amx);
+        amax_flush(p.amax_out + tc.g * p.alpha_group_stride, amx, alpha, OUT_BF16);
+      }
       const int64_t row = (int64_t)tc.mt * BM + 32 * q + lane;
       if (row >= p.M) continue;
 #pragma unroll
@@ -699,6 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #endif
       const int64_t row = (int64_t)tc.mt * 256 + 128 * rank + 32 * q + lane;
       const int64_t colh = (int64_t)tc.nt * BN + 128 * h;
+      float amx = 0.f;  // producer-fused amax of this warp's 32 x 128 slice
       if (OUT_BF16 == 1) {
         // TMEM -> registers -> bf16 -> this warp's 128-byte-swizzled staging
         // slice (32 rows x 128 columns = two TMA boxes); release TMEM, then
@@ -718,6 +758,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
           }
+          if (p.amax_out) amx = absmax32(r, amx);
           uint32_t w[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
@@ -760,6 +801,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           tma_store_3d(&tmap_c, stage, col + 64, rowb, tc.g);
           bulk_commit();
         }
+        if (p.amax_out) amax_flush(p.amax_out + tc.g * p.alpha_group_stride, amx, alpha, true);
         continue;
       } else if (OUT_BF16 == 2) {
         // f32: chunk 0 staged in this warp's 32x32 f32 box, chunks 1-3 kept in
@@ -782,6 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
           if (i == 0) {
+            if (p.amax_out) amx = absmax32(r, amx);  // stored values; chunks 1-3 below
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               sts128(box + ((j ^ (lane & 7)) << 4), r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
@@ -795,6 +838,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (i > 0) {
+            if (p.amax_out) amx = absmax32(keep[i - 1], amx);
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
 #pragma unroll
@@ -809,6 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             bulk_commit();
           }
         }
+        if (p.amax_out) amax_flush(p.amax_out + tc.g * p.alpha_group_stride, amx, 1.f, false);
         continue;
       } else {
         // f32: store each 32-column slice as soon as it is loaded, release after the last
@@ -824,6 +869,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
           }
+          if (p.amax_out) amx = absmax32(r, amx);
           if (row >= p.M) continue;
           if (vec) {
 #pragma unroll
@@ -836,6 +882,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
               if (colh + 32 * i + j < p.N) out[32 * i + j] = __uint_as_float(r[j]) * alpha;
           }
         }
+        if (p.amax_out) amax_flush(p.amax_out + tc.g * p.alpha_group_stride, amx, alpha, false);
       }
     }
   }
@@ -918,7 +965,7 @@ bool make_out_map(CUtensorMap* m, void* c, int64_t groups, int64_t M, int64_t N,
 int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const double* alpha_a,
                 const uint8_t* b_codes, const uint8_t* b_sf, const double* alpha_b, int64_t M,
                 int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype, int alpha_per_group,
-                cudaStream_t stream) {
+                double* amax_out, cudaStream_t stream) {
   if (!a_codes || !a_sf || !alpha_a || !b_codes || !b_sf || !alpha_b || !c) return F46_ERR_INVALID_ARG;
   if (groups < 1 || M <= 0 || N <= 0 || K <= 0 || ldc < N) return F46_ERR_INVALID_ARG;
   if (c_dtype != F46_DT_F32 && c_dtype != F46_DT_BF16) return F46_ERR_INVALID_ARG;
@@ -947,6 +994,7 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   p.c_group_stride = M * ldc;
   p.alpha_group_stride = alpha_per_group ? 1 : 0;
   p.c_bf16 = c_dtype == F46_DT_BF16;
+  p.amax_out = amax_out;
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -1042,7 +1090,16 @@ int f46_gemm_nvfp4(const uint8_t* a_codes, const uint8_t* a_scales_tc, const dou
                    int64_t M, int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
                    f46_stream_t stream) {
   return gemm_launch(1, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M, N, K,
-                     c, ldc, c_dtype, 0, (cudaStream_t)stream);
+                     c, ldc, c_dtype, 0, nullptr, (cudaStream_t)stream);
+}
+
+int f46_gemm_nvfp4_amax(const uint8_t* a_codes, const uint8_t* a_scales_tc, const double* d_alpha_a,
+                        const uint8_t* b_codes, const uint8_t* b_scales_tc, const double* d_alpha_b,
+                        int64_t M, int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                        double* d_amax_out, f46_stream_t stream) {
+  if (!d_amax_out) return F46_ERR_INVALID_ARG;
+  return gemm_launch(1, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M, N, K,
+                     c, ldc, c_dtype, 0, d_amax_out, (cudaStream_t)stream);
 }
 
 int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
@@ -1051,7 +1108,17 @@ int f46_gemm_nvfp4_grouped(int groups, const uint8_t* a_codes, const uint8_t* a_
                            int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
                            f46_stream_t stream) {
   return gemm_launch(groups, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M,
-                     N, K, c, ldc, c_dtype, 1, (cudaStream_t)stream);
+                     N, K, c, ldc, c_dtype, 1, nullptr, (cudaStream_t)stream);
+}
+
+int f46_gemm_nvfp4_grouped_amax(int groups, const uint8_t* a_codes, const uint8_t* a_scales_tc,
+                                const double* d_alpha_a, const uint8_t* b_codes,
+                                const uint8_t* b_scales_tc, const double* d_alpha_b, int64_t M,
+                                int64_t N, int64_t K, void* c, int64_t ldc, int c_dtype,
+                                double* d_amax_out, f46_stream_t stream) {
+  if (!d_amax_out) return F46_ERR_INVALID_ARG;
+  return gemm_launch(groups, a_codes, a_scales_tc, d_alpha_a, b_codes, b_scales_tc, d_alpha_b, M,
+                     N, K, c, ldc, c_dtype, 1, d_amax_out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

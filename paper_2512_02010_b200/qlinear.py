@@ -37,8 +37,13 @@ def round_to_bf16(x: torch.Tensor) -> torch.Tensor:
 
 
 def gemm_nvfp4(aq: QuantizedTensor, bq: QuantizedTensor, out_dtype=torch.float32,
-               out: torch.Tensor | None = None) -> torch.Tensor:
-    """C[M,N] = dequant(aq) @ dequant(bq)^T on tcgen05 (both blocked along K)."""
+               out: torch.Tensor | None = None,
+               amax_out: torch.Tensor | None = None) -> torch.Tensor:
+    """C[M,N] = dequant(aq) @ dequant(bq)^T on tcgen05 (both blocked along K).
+
+    ``amax_out`` (a float64 CUDA tensor of one element): the epilogue also
+    writes max |C| of the stored values into it (producer-fused amax), ready to
+    pass as ``d_amax=`` to the next quantize so it skips its amax pass."""
     L = _lib.load()
     if len(aq.shape) != 2 or len(bq.shape) != 2:
         raise InvalidInputError("the NVFP4 GEMM is defined for 2-D operands")
@@ -57,25 +62,50 @@ def gemm_nvfp4(aq: QuantizedTensor, bq: QuantizedTensor, out_dtype=torch.float32
         a_codes = torch.nn.functional.pad(a_codes, (0, 8))
         b_codes = torch.nn.functional.pad(b_codes, (0, 8))
         k_eff = (-(-K // 16) + 1) * 16
-    rc = L.f46_gemm_nvfp4(a_codes.data_ptr(), aq.scales_tc.data_ptr(),
-                          aq.alpha_dev.data_ptr(), b_codes.data_ptr(),
-                          bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, k_eff,
-                          out.data_ptr(), out.stride(0), dt, _stream())
+    if amax_out is None:
+        rc = L.f46_gemm_nvfp4(a_codes.data_ptr(), aq.scales_tc.data_ptr(),
+                              aq.alpha_dev.data_ptr(), b_codes.data_ptr(),
+                              bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, k_eff,
+                              out.data_ptr(), out.stride(0), dt, _stream())
+    else:
+        _check_amax_buffer(amax_out, 1, dev)
+        amax_out.zero_()
+        rc = L.f46_gemm_nvfp4_amax(a_codes.data_ptr(), aq.scales_tc.data_ptr(),
+                                   aq.alpha_dev.data_ptr(), b_codes.data_ptr(),
+                                   bq.scales_tc.data_ptr(), bq.alpha_dev.data_ptr(), M, N, k_eff,
+                                   out.data_ptr(), out.stride(0), dt, amax_out.data_ptr(),
+                                   _stream())
     _lib.check(rc, "f46_gemm_nvfp4")
     return out
 
 
+def _check_amax_buffer(t: torch.Tensor, n: int, dev) -> None:
+    if (not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or t.numel() != n
+            or t.device != dev or not t.is_contiguous()):
+        raise InvalidInputError(f"amax_out must be a contiguous float64 CUDA tensor of {n} "
+                                "element(s) on the operands' device")
+
+
 def gemm_nvfp4_grouped(a_codes, a_scales, a_alpha, b_codes, b_scales, b_alpha, M, N, K,
-                       out_dtype=torch.float32) -> torch.Tensor:
+                       out_dtype=torch.float32, amax_out: torch.Tensor | None = None) -> torch.Tensor:
     """G independent GEMMs of one shape (MoE experts): operands packed back to
-    back ([G, ...] device tensors), one alpha per group, C is [G, M, N]."""
+    back ([G, ...] device tensors), one alpha per group, C is [G, M, N].
+    ``amax_out`` (float64 [G]): per-group max |C| from the epilogue."""
     L = _lib.load()
     G = a_codes.shape[0]
     dt = {torch.float32: _lib.DT_F32, torch.bfloat16: _lib.DT_BF16}[out_dtype]
     out = torch.empty((G, M, N), dtype=out_dtype, device=a_codes.device)
-    rc = L.f46_gemm_nvfp4_grouped(G, a_codes.data_ptr(), a_scales.data_ptr(), a_alpha.data_ptr(),
-                                  b_codes.data_ptr(), b_scales.data_ptr(), b_alpha.data_ptr(),
-                                  M, N, K, out.data_ptr(), N, dt, _stream())
+    if amax_out is None:
+        rc = L.f46_gemm_nvfp4_grouped(G, a_codes.data_ptr(), a_scales.data_ptr(),
+                                      a_alpha.data_ptr(), b_codes.data_ptr(), b_scales.data_ptr(),
+                                      b_alpha.data_ptr(), M, N, K, out.data_ptr(), N, dt, _stream())
+    else:
+        _check_amax_buffer(amax_out, G, a_codes.device)
+        amax_out.zero_()
+        rc = L.f46_gemm_nvfp4_grouped_amax(G, a_codes.data_ptr(), a_scales.data_ptr(),
+                                           a_alpha.data_ptr(), b_codes.data_ptr(),
+                                           b_scales.data_ptr(), b_alpha.data_ptr(), M, N, K,
+                                           out.data_ptr(), N, dt, amax_out.data_ptr(), _stream())
     _lib.check(rc, "f46_gemm_nvfp4_grouped")
     return out
 

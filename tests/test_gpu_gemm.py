@@ -165,3 +165,46 @@ def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
     assert torch.equal(fast, strided)
     assert torch.equal(fast, simple), "CTA-pair and single-CTA kernels differ"
     assert rel_fro(fast.float(), gpu_oracle(aq, bq)) <= (REL_TOL if out_dtype == torch.float32 else 4e-3)
+
+
+@pytest.mark.parametrize("kernel", ["pair", "1sm", "simple"])
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("M,N,K", [(700, 1000, 1024), (256, 512, 256), (33, 40, 48)])
+def test_producer_fused_amax(M, N, K, out_dtype, kernel, monkeypatch):
+    """The epilogue's amax equals max |C| of the stored tensor exactly (every
+    kernel, every output type, ragged tiles) and, handed to the next quantize
+    as its amax, yields the container K1 + K2 produce."""
+    if kernel == "1sm":
+        monkeypatch.setenv("F46_GEMM_1SM", "1")
+    elif kernel == "simple":
+        monkeypatch.setenv("F46_GEMM_SIMPLE", "1")
+    aq = f46.quantize_tensor_adaptive(bf16_randn((M, K), 81).cuda(), ADAPT)
+    bq = f46.quantize_tensor_adaptive(bf16_randn((N, K), 82).cuda(), ADAPT)
+    amax = torch.full((1,), 123.0, dtype=torch.float64, device="cuda")  # zeroed by the call
+    c = f46.gemm_nvfp4(aq, bq, out_dtype, amax_out=amax)
+    assert torch.equal(c, f46.gemm_nvfp4(aq, bq, out_dtype))
+    assert float(amax) == float(c.abs().max().double())
+    if out_dtype == torch.bfloat16 and c.shape[1] % 16 == 0:
+        fused = f46.quantize_tensor_adaptive(c, ADAPT, d_amax=amax)
+        plain = f46.quantize_tensor_adaptive(c, ADAPT)
+        assert fused.alpha == plain.alpha
+        assert torch.equal(fused.packed_codes, plain.packed_codes)
+        assert torch.equal(fused.scales_tc, plain.scales_tc)
+
+
+def test_grouped_amax_per_group():
+    G, M, N, K = 3, 300, 256, 256
+    qa = [f46.quantize_tensor_adaptive(bf16_randn((M, K), 300 + i, std=1.0 + i).cuda(), ADAPT)
+          for i in range(G)]
+    qb = [f46.quantize_tensor_adaptive(bf16_randn((N, K), 400 + i).cuda(), ADAPT) for i in range(G)]
+    st = lambda xs: torch.stack(xs)
+    amax = torch.empty(G, dtype=torch.float64, device="cuda")
+    out = f46.gemm_nvfp4_grouped(st([q.packed_codes for q in qa]), st([q.scales_tc for q in qa]),
+                                 torch.cat([q.alpha_dev for q in qa]),
+                                 st([q.packed_codes for q in qb]), st([q.scales_tc for q in qb]),
+                                 torch.cat([q.alpha_dev for q in qb]), M, N, K, torch.bfloat16,
+                                 amax_out=amax)
+    for g in range(G):
+        assert float(amax[g]) == float(out[g].abs().max().double())
+    with pytest.raises(f46.InvalidInputError):
+        f46.gemm_nvfp4(qa[0], qb[0], amax_out=torch.zeros(2, dtype=torch.float64, device="cuda"))
