@@ -207,6 +207,9 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_MINB
 #define F46_MINB 4
 #endif
+#ifndef F46_UNCOND_STORE
+#define F46_UNCOND_STORE 0
+#endif
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {
@@ -416,6 +419,18 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         float bmax;
         load_block<DT>(blk_addr, x, bmax);
         BlockOut o;
+#if F46_UNCOND_STORE
+        // straight line: store unconditionally; a deferred block's bytes are
+        // rewritten by the resolve pass (ordered after this by __syncwarp)
+        const bool ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
+        *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
+        sptr[j * 4096] = (uint8_t)o.sc;
+        if constexpr (EXTRA) {
+          if (p.scales_rm) p.scales_rm[rbk + lane + 32 * j] = (uint8_t)o.sc;
+          if (p.pick4) p.pick4[rbk + lane + 32 * j] = (uint8_t)o.pick4;
+        }
+        fails |= (ok ? 0u : 1u) << j;
+#else
         if (block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o)) {
           *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
           sptr[j * 4096] = (uint8_t)o.sc;
@@ -426,6 +441,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         } else {
           fails |= 1u << j;
         }
+#endif
       };
       if (nbs == kSegBlocks) {
 #pragma unroll kKbUnroll
