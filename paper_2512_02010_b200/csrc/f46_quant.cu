@@ -201,14 +201,14 @@ constexpr int kWarps = 4;
 #endif
 constexpr int kSegElems = F46_SEG;
 #ifndef F46_KB_UNROLL
-#define F46_KB_UNROLL 1
+#define F46_KB_UNROLL 4
 #endif
 constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_MINB
 #define F46_MINB 4
 #endif
 #ifndef F46_UNCOND_STORE
-#define F46_UNCOND_STORE 0
+#define F46_UNCOND_STORE 1
 #endif
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
