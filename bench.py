@@ -180,6 +180,26 @@ def run_reference(args):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+class L2Flush:
+    """Evict L2 between timed steps without leaving it dirty: write 256 MB (>
+    the 126 MB L2), then sweep-read another 256 MB so the written lines are
+    written back *before* the timed region.  A write-only flush leaves ~126 MB
+    of dirty lines whose write-back would be charged to the next kernel."""
+
+    def __init__(self, dev):
+        import torch
+
+        self.w = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+        self.r = torch.ones(128 * 1024 * 1024, dtype=torch.float16, device=dev)
+        self.sink = None
+
+    def __call__(self, i=0):
+        import torch
+
+        self.w.fill_(i & 0xFF)
+        self.sink = torch.amax(self.r)
+
+
 def _events(n):
     import torch
     return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
@@ -209,7 +229,7 @@ def run_b200(args):
     elems_local = x.numel()
     elems_total = ROWS * COLS
     stream = torch.cuda.current_stream()
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_buf = L2Flush(dev)
 
     codes = torch.empty((rows_local, COLS // 2), dtype=torch.uint8, device=dev)
     scales = torch.empty(scales_tc_bytes(rows_local, COLS), dtype=torch.uint8, device=dev)
@@ -240,7 +260,7 @@ def run_b200(args):
 
     warmup = max(args.warmup, 3)
     for _ in range(warmup):
-        flush_buf.fill_(1)
+        flush_buf(1)
         step()
     barrier()
 
@@ -250,7 +270,7 @@ def run_b200(args):
     starts, ends = _events(args.steps), _events(args.steps)
     barrier()
     for i in range(args.steps):
-        flush_buf.fill_(i & 0xFF)  # evict L2 (256 MB > 126 MB) outside the timed span
+        flush_buf(i)  # evict L2 (clean) outside the timed span
         torch.cuda._sleep(200_000)  # device busy while the host enqueues the step
         starts[i].record(stream)
         step(i)
@@ -316,7 +336,7 @@ def run_b200(args):
         "data": "synthetic (torch.randn N(0,1) -> bf16)",
         "config": {"workload": WORKLOAD, "rows": ROWS, "cols": COLS, "rows_per_rank": rows_local,
                    "mode": "adaptive", "parallelism": f"row-shard x{world} + NCCL allreduce(MAX)",
-                   "l2": "flushed (256 MB write) before every timed step; input 512 MB > L2",
+                   "l2": "flushed before every timed step (256 MB write + 256 MB read sweep: L2 cold and clean); input 512 MB > L2",
                    "bytes_per_elem": BYTES_PER_ELEM},
         "roofline": roofline, "e2e": e2e,
         "gpu_launches": 2 * args.steps,
@@ -342,13 +362,13 @@ def bench_dequant(args, L, dev, peaks, codes, scales, alpha, rows):
     from paper_2512_02010_b200 import _lib
 
     stream = torch.cuda.current_stream()
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_buf = L2Flush(dev)
     out = {}
     for od, code, ob in ((torch.bfloat16, _lib.DT_BF16, 2), (torch.float32, _lib.DT_F32, 4)):
         y = torch.empty((rows, COLS), dtype=od, device=dev)
         ts = []
         for i in range(max(5, args.steps) + 3):
-            flush_buf.fill_(i & 0xFF)
+            flush_buf(i)
             torch.cuda._sleep(200_000)
             s, e = _events(2)
             s.record(stream)
@@ -374,7 +394,7 @@ def bench_weights(args, L, dev, peaks):
     from paper_2512_02010_b200.blockquant import scales_tc_bytes
 
     stream = torch.cuda.current_stream()
-    flush_buf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush_buf = L2Flush(dev)
     out = {}
     for (r, c) in [(4096, 4096), (4096, 14336), (14336, 4096)]:
         g = torch.Generator(device=dev).manual_seed(r * 7 + c)
@@ -394,7 +414,7 @@ def bench_weights(args, L, dev, peaks):
             once()
         ts = []
         for i in range(max(5, args.steps)):
-            flush_buf.fill_(i & 0xFF)
+            flush_buf(i)
             # keep the GPU busy while the host enqueues: the timed region is
             # device time of the three launches, not the host's launch latency
             torch.cuda._sleep(200_000)

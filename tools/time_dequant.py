@@ -15,6 +15,7 @@ g = torch.Generator(device=dev).manual_seed(5)
 codes = torch.randint(0, 256, (rows, cols // 2), generator=g, device=dev, dtype=torch.uint8)
 scales = torch.randint(0, 0x7E, (scales_tc_bytes(rows, cols),), generator=g, device=dev, dtype=torch.uint8)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+flush_r = torch.ones(128 << 20, dtype=torch.float16, device=dev)  # read sweep: leaves L2 clean
 s = torch.cuda.current_stream().cuda_stream
 
 
@@ -22,6 +23,7 @@ def timed(fn, n=15):
     ts = []
     for i in range(n):
         flush.fill_(i)
+        sink = torch.amax(flush_r)
         torch.cuda._sleep(200_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
