@@ -372,27 +372,43 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 
   // Each warp streams one contiguous range of tiles (tile = one segment of one
   // row): successive tiles are adjacent in memory, so cursors only step.
+  // The tiles tile the flat input contiguously, so the issue cursor is one
+  // pointer that advances by the tile's size (lane 0 only).
+  const uint32_t last_n = cols - (n_seg - 1) * kSegElems;  // elements in a row's last segment
+  // (Byte offsets are 32-bit: the host launches at most 2^31 input bytes at a time.)
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
-  uint32_t irow = t_begin / n_seg, iseg = t_begin - irow * n_seg;  // next tile to issue
-  uint32_t tnext = t_begin;
+  uint32_t iseg, tnext = t_begin, src;
+  {
+    const uint32_t irow = t_begin / n_seg;
+    iseg = t_begin - irow * n_seg;
+    src = (irow * cols + iseg * kSegElems) * kEsz;
+  }
   auto issue = [&](int s) {
+    const uint32_t n = (iseg == n_seg - 1) ? last_n : (uint32_t)kSegElems;
     if (tnext < t_end) {
-      const uint32_t c0 = iseg * kSegElems;
-      const uint32_t n = min((uint32_t)kSegElems, cols - c0);
       mbar_expect_tx(&wb[s], n * kEsz);
-      bulk_load(wsm + s * kTileBytes, xb + ((uint64_t)irow * cols + c0) * kEsz, n * kEsz, &wb[s]);
+      bulk_load(wsm + s * kTileBytes, xb + src, n * kEsz, &wb[s]);
     }
+    src += n * kEsz;
     ++tnext;
-    if (++iseg == n_seg) {
-      iseg = 0;
-      ++irow;
-    }
+    if (++iseg == n_seg) iseg = 0;
   };
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) issue(s);
   }
   uint32_t row = t_begin / n_seg, seg = t_begin - row * n_seg;  // tile being consumed
+  // Per-lane output cursors, stepped per tile: lane l owns blocks kb0 + l + 32j,
+  // whose codes sit 256 B apart (the codes of consecutive tiles are contiguous)
+  // and whose tcgen05-layout scales sit 8 atoms (4 KB) apart; a tile advances
+  // the scale cursor by kSegBlocks/4 atoms within a row and is recomputed at a
+  // row change.
+  auto sf_cursor = [&](uint32_t r, uint32_t kb0) -> uint32_t {
+    return ((r >> 7) * kb4 + (kb0 >> 2) + (lane >> 2)) * 512 + (r & 31) * 16 +
+           ((r & 127) >> 5) * 4 + (lane & 3);
+  };
+  uint32_t coff = (row * nb + seg * kSegBlocks + lane) * 8;
+  uint32_t soff = sf_cursor(row, seg * kSegBlocks);
 
   uint32_t t = t_begin;
   int s = 0;
@@ -405,12 +421,6 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
       const uint32_t kb0 = seg * kSegBlocks;                // a multiple of 4
       const uint32_t nbs = min(kSegBlocks, nb - kb0);       // blocks in this segment
       const uint64_t rbk = (uint64_t)row * nb + kb0;        // first block of the segment
-      // Per-lane output cursors: lane l owns blocks kb0 + l + 32j, whose codes
-      // sit 256 B apart and whose tcgen05-layout scales sit 8 tiles (4 KB) apart.
-      uint8_t* cptr = p.codes + (rbk + lane) * 8;
-      uint8_t* sptr = p.scales_tc +
-                      ((uint64_t)(row >> 7) * kb4 + (kb0 >> 2) + (lane >> 2)) * 512 +
-                      (row & 31) * 16 + ((row & 127) >> 5) * 4 + (lane & 3);
       const uint32_t blk0 = wsm + s * kTileBytes + lane * (16 * kEsz);
       uint32_t fails = 0;
       auto one = [&](int j) {
@@ -423,8 +433,8 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         // straight line: store unconditionally; a deferred block's bytes are
         // rewritten by the resolve pass (ordered after this by __syncwarp)
         const bool ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
-        *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
-        sptr[j * 4096] = (uint8_t)o.sc;
+        *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
+        p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
         if constexpr (EXTRA) {
           if (p.scales_rm) p.scales_rm[rbk + lane + 32 * j] = (uint8_t)o.sc;
           if (p.pick4) p.pick4[rbk + lane + 32 * j] = (uint8_t)o.pick4;
@@ -432,8 +442,8 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         fails |= (ok ? 0u : 1u) << j;
 #else
         if (block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o)) {
-          *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
-          sptr[j * 4096] = (uint8_t)o.sc;
+          *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
+          p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
           if constexpr (EXTRA) {
             if (p.scales_rm) p.scales_rm[rbk + lane + 32 * j] = (uint8_t)o.sc;
             if (p.pick4) p.pick4[rbk + lane + 32 * j] = (uint8_t)o.pick4;
@@ -465,9 +475,13 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         s = 0;
         parity ^= 1u;
       }
+      coff += nbs * 8;
       if (++seg == n_seg) {
         seg = 0;
         ++row;
+        soff = sf_cursor(row, 0);
+      } else {
+        soff += (kSegBlocks / 4) * 512;
       }
     }
     // ---- deferred blocks: exact float64 path (outside the hot loop) ----
@@ -1765,11 +1779,31 @@ int launch_quant_seg(const QParams& p, cudaStream_t s) {
     if (ctas_per_sm < 1) ctas_per_sm = 1;
     configured = true;
   }
-  const int64_t tiles = p.rows * ((p.cols + kSegElems - 1) / kSegElems);
-  int64_t grid = (tiles + kWarps - 1) / kWarps;
-  if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
-  if (grid < 1) grid = 1;
-  quant_seg_kernel<DT, MODE, EXTRA><<<(unsigned)grid, kWarps * 32, smem, s>>>(p);
+  // The kernel keeps 32-bit byte offsets: launch at most 2^31 input bytes at a
+  // time, in whole 128-row slabs so each launch owns complete scale atoms.
+  constexpr int64_t kEsz = (DT == DT_BF16) ? 2 : 4;
+  const int64_t nb = p.cols >> 4, kb4 = (nb + 3) >> 2;
+  int64_t chunk_bytes = (int64_t)1 << 31;
+  if (const char* e = getenv("F46_SEG_CHUNK_BYTES")) {  // test hook: force multi-launch
+    const long long v = atoll(e);
+    if (v > 0 && v < chunk_bytes) chunk_bytes = v;
+  }
+  int64_t rows_max = (chunk_bytes / (p.cols * kEsz)) & ~(int64_t)127;
+  if (rows_max < 128) return F46_ERR_UNSUPPORTED;
+  for (int64_t r0 = 0; r0 < p.rows; r0 += rows_max) {
+    QParams q = p;
+    q.rows = std::min(rows_max, p.rows - r0);
+    q.x = reinterpret_cast<const uint8_t*>(p.x) + r0 * p.cols * kEsz;
+    q.codes = p.codes + r0 * nb * 8;
+    q.scales_tc = p.scales_tc + (r0 / 128) * kb4 * 512;
+    if (p.scales_rm) q.scales_rm = p.scales_rm + r0 * nb;
+    if (p.pick4) q.pick4 = p.pick4 + r0 * nb;
+    const int64_t tiles = q.rows * ((q.cols + kSegElems - 1) / kSegElems);
+    int64_t grid = (tiles + kWarps - 1) / kWarps;
+    if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
+    if (grid < 1) grid = 1;
+    quant_seg_kernel<DT, MODE, EXTRA><<<(unsigned)grid, kWarps * 32, smem, s>>>(q);
+  }
   return launch_status();
 }
 

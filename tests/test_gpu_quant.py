@@ -192,3 +192,18 @@ def test_dequant_flat_paths_ragged(shape, alpha, path, monkeypatch):
     assert np.array_equal(d32, d64.astype(np.float32))
     d16 = f46.dequantize_tensor(q, torch.bfloat16).cpu().view(torch.int16).numpy().view(np.uint16)
     assert np.array_equal(d16, f64_to_bf16_bits(d64))
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6"])
+def test_k2_multi_launch_row_slabs(mode, monkeypatch):
+    """K2 keeps 32-bit offsets and launches at most 2^31 input bytes at a time
+    in 128-row slabs; forcing 1 MB slabs (4 launches + a ragged last slab)
+    gives the single-launch container bit for bit."""
+    x = bf16_randn((1000, 512), 5).cuda()
+    ref = run(x, mode)
+    monkeypatch.setenv("F46_SEG_CHUNK_BYTES", str(1 << 18))
+    got = run(x, mode)
+    assert got.alpha == ref.alpha
+    assert torch.equal(got.packed_codes, ref.packed_codes)
+    assert torch.equal(got.scales_tc, ref.scales_tc)
+    assert torch.equal(got.pick4, ref.pick4) and torch.equal(got.scales_rm, ref.scales_rm)
