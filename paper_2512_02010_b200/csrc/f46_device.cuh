@@ -37,6 +37,9 @@
 #ifndef F46_PRMT_LO
 #define F46_PRMT_LO 0
 #endif
+#ifndef F46_NEWTON
+#define F46_NEWTON 0
+#endif
 
 namespace f46 {
 
@@ -606,6 +609,27 @@ __device__ __forceinline__ uint64_t codes_newton(const float2 (&x)[8], float D, 
   return ((uint64_t)w1 << 32) | w0;
 }
 
+// TDIR == 0 again (BF16 x: <= 8 significant bits; D = alpha*Delta exact),
+// cheaper than the Newton step: split 1/D as Rhi + Rlo with Rhi truncated to
+// 16 significant bits, so x*Rhi is exact in f32 (8 + 16 bits) and
+// q0 = fma(x, Rlo, x*Rhi) is ONE rounding of x*(Rhi + Rlo) = q*(1 + e),
+// |e| <= 2^-37 (Rlo = fma(-D, Rhi, 1)*R carries R's 2^-22 error on a 2^-16
+// remainder).  An exact tie t therefore comes out as t exactly and every
+// other quotient stays on its side of every tie (>= 2^-16.3 away), so
+// cvt.rn's ties-to-even is the reference's rounding.  x = -0 stays -0.
+__device__ __forceinline__ uint64_t codes_split(const float2 (&x)[8], float D) {
+  const float R = rcp_approx(D);
+  const float Rhi = __uint_as_float(__float_as_uint(R) & 0xFFFFFF00u);
+  const float Rlo = fmaf(-D, Rhi, 1.0f) * R;
+  const float2 H2 = make_float2(Rhi, Rhi), L2 = make_float2(Rlo, Rlo);
+  float2 q[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) q[p] = __ffma2_rn(x[p], L2, __fmul2_rn(x[p], H2));
+  const uint32_t w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  const uint32_t w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]);
+  return ((uint64_t)w1 << 32) | w0;
+}
+
 template <int TDIR, class Load>
 __device__ __forceinline__ uint64_t codes_dir(const float2 (&x)[8], float rq, float D,
                                               float alpha, float delta, const Load& load) {
@@ -614,7 +638,11 @@ __device__ __forceinline__ uint64_t codes_dir(const float2 (&x)[8], float rq, fl
   } else if constexpr (TDIR == 1) {
     return codes_of(x, rq * F46_QHI_OVER_QLO);
   } else if constexpr (TDIR == 0) {
+#if F46_NEWTON
     return codes_newton(x, D, rq);
+#else
+    return codes_split(x, D);
+#endif
   } else {
     return exact_codes(x, rq, alpha, delta, TDIR, load);
   }
