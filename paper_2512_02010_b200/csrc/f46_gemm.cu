@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // have pulled it into registers (128 f32 columns per thread); scaling,
 // conversion and the global stores then overlap the next tile's MMAs.
 // ---------------------------------------------------------------------------
+#ifndef F46_EPI_BATCH
+#define F46_EPI_BATCH 1
+#endif
 #ifndef F46_GEMM_DEBUG
 #define F46_GEMM_DEBUG 0
 #endif
@@ -748,16 +751,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         if (lane == 0) bulk_wait_read<0>();  // previous tile's store has read the box
         __syncwarp();
         uint32_t keep[2][16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t r[32];
-          tc_ld_32x32b_x32(taddr + 32 * i, r);
-          tc_wait_ld();
-          if (i == 3) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
-          }
+        // chunk -> bf16 words -> staging box (chunks 0-1) or registers (2-3)
+        auto emit = [&](const uint32_t (&r)[32], int i) {
           if (p.amax_out) amx = absmax32(r, amx);
           uint32_t w[16];
 #pragma unroll
@@ -776,13 +771,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #pragma unroll
             for (int k = 0; k < 16; ++k) keep[i - 2][k] = w[k];
           }
+        };
+#if F46_GEMM_DEBUG == 9
+        // timing probe (wrong results): release TMEM before draining it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+#endif
+#if F46_EPI_BATCH
+        // two TMEM loads per wait: the accumulator is drained in two round trips
+        {
+          uint32_t ra[32], rb[32];
+          tc_ld_32x32b_x32(taddr, ra);
+          tc_ld_32x32b_x32(taddr + 32, rb);
+          tc_wait_ld();
+          emit(ra, 0);
+          emit(rb, 1);
+          tc_ld_32x32b_x32(taddr + 64, ra);
+          tc_ld_32x32b_x32(taddr + 96, rb);
+          tc_wait_ld();
+#if F46_GEMM_DEBUG != 9
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+#endif
+          emit(ra, 2);
+          emit(rb, 3);
         }
+#else
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[32];
+          tc_ld_32x32b_x32(taddr + 32 * i, r);
+          tc_wait_ld();
+          if (i == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+          }
+          emit(r, i);
+        }
+#endif
         const int col = tc.nt * BN + 128 * h;
         const int rowb = tc.mt * 256 + 128 * (int)rank + 32 * q;
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
+#if F46_GEMM_DEBUG != 8
           tma_store_3d(&tmap_c, stage, col, rowb, tc.g);
+#endif
           bulk_commit();
           bulk_wait_read<0>();
         }
@@ -798,7 +835,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
+#if F46_GEMM_DEBUG != 8
           tma_store_3d(&tmap_c, stage, col + 64, rowb, tc.g);
+#endif
           bulk_commit();
         }
         if (p.amax_out) amax_flush(p.amax_out + tc.g * p.alpha_group_stride, amx, alpha, true);
@@ -811,27 +850,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
         uint32_t keep[3][32];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        {
+          // two TMEM loads per wait; chunks 1-3 land straight in `keep`
           uint32_t r[32];
-          tc_ld_32x32b_x32(taddr + 32 * i, r);
+          tc_ld_32x32b_x32(taddr, r);
+          tc_ld_32x32b_x32(taddr + 32, keep[0]);
           tc_wait_ld();
-          if (i == 3) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
-          }
 #pragma unroll
           for (int k = 0; k < 32; ++k) r[k] = __float_as_uint(__uint_as_float(r[k]) * alpha);
-          if (i == 0) {
-            if (p.amax_out) amx = absmax32(r, amx);  // stored values; chunks 1-3 below
+          if (p.amax_out) amx = absmax32(r, amx);  // stored values; chunks 1-3 below
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              sts128(box + ((j ^ (lane & 7)) << 4), r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
-          } else {
+          for (int j = 0; j < 8; ++j)
+            sts128(box + ((j ^ (lane & 7)) << 4), r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+          tc_ld_32x32b_x32(taddr + 64, keep[1]);
+          tc_ld_32x32b_x32(taddr + 96, keep[2]);
+          tc_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) keep[i - 1][k] = r[k];
-          }
+          for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              keep[i][k] = __float_as_uint(__uint_as_float(keep[i][k]) * alpha);
         }
         const int col = tc.nt * BN + 128 * h;
         const int rowb = tc.mt * 256 + 128 * (int)rank + 32 * q;

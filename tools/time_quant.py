@@ -25,8 +25,9 @@ mcap = {"adaptive": 1536.0, "fixed6": 2688.0, "fixed4": 1792.0}[mode]
 L.f46_amax(x.data_ptr(), DT, x.numel(), amax.data_ptr(), s)
 ts = []
 for i in range(25):
-    flush.fill_(i)
-    sink = torch.amax(flush_r)
+    if not os.environ.get("NOFLUSH"):
+        flush.fill_(i)
+        sink = torch.amax(flush_r)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     L.f46_quantize(x.data_ptr(), DT, rows, cols, _lib.MODE[mode], 0, mcap, amax.data_ptr(), 0.0,
