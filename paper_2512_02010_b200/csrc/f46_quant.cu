@@ -1926,7 +1926,9 @@ int f46_amax(const void* x, int dtype, int64_t n, double* d_amax, f46_stream_t s
   if (!x || !d_amax || n < 0) return F46_ERR_INVALID_ARG;
   if (n == 0) return F46_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t per = dtype == F46_DT_BF16 ? 256 * 8 * 4 : 256 * 4 * 4;
+  // >= 16 vectors of 16 bytes per thread: small tensors get fewer CTAs and so
+  // fewer same-address atomics at the tail; large ones the full 8 CTAs per SM
+  const int64_t per = dtype == F46_DT_BF16 ? 256 * 8 * 16 : 256 * 4 * 16;
   int64_t grid = (n + per - 1) / per;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;
