@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // have pulled it into registers (128 f32 columns per thread); scaling,
 // conversion and the global stores then overlap the next tile's MMAs.
 // ---------------------------------------------------------------------------
+#ifndef F46_SFA_DIAG
+#define F46_SFA_DIAG 1
+#endif
 #ifndef F46_EPI_BATCH
 #define F46_EPI_BATCH 1
 #endif
@@ -621,10 +624,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int s = it % kStagesPair;
           if (it >= kStagesPair) mbar_wait(&empty[s], ((it / kStagesPair) - 1) & 1);
+#if F46_GEMM_DEBUG == 10
+          if (leader) mbar_arrive(&full[s]);  // timing probe: no operand traffic
+#else
           if (leader) mbar_expect_tx(&full[s], 2 * (PA_BYTES + PB_BYTES));
           const uint32_t bar = smem_u32(&full[s]);
           tma_load_3d_pair(smem_u32(sm_a + s * PA_BYTES), &tmap_a, bar, kt * (BK / 2), m0, tc.g);
           tma_load_3d_pair(smem_u32(sm_b + s * PB_BYTES), &tmap_b, bar, kt * (BK / 2), nb0, tc.g);
+#endif
           mbar_expect_tx(&sf_ld_full[s], PSFA_BYTES + PSFB_BYTES);
           tma_load_3d(smem_u32(sm_sfa + s * PSFA_BYTES), &tmap_sfa, &sf_ld_full[s], 0,
                       sfa_row + 8 * kt, tc.g);
@@ -713,7 +720,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
           }
         }
         const uint32_t tsfa = lane_taddr + TM_SF + b * TM_SF_BUF;
+#if F46_SFA_DIAG
+        // the MMA reads row block q's SFA from this quadrant at column 4j + q
+        // only: write that column, not all four replicas
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tc_st_32x32b_x1(tsfa + 4 * j + q, va[4 * j]);
+#else
         tc_st_32x32b_x16(tsfa, va);
+#endif
         tc_st_32x32b_x32(tsfa + 16, vb);
         tc_wait_st();
         tc_fence_before();

@@ -241,6 +241,9 @@ __device__ __forceinline__ void mma_nvf4_pair(uint32_t tmem_d, uint64_t adesc, u
 
 
 // register -> TMEM stores of this warp's 32 lanes (columns starting at taddr)
+__device__ __forceinline__ void tc_st_32x32b_x1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void tc_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
