@@ -363,6 +363,7 @@ def run_b200(args):
         line["weights"] = bench_weights(args, L, dev, peaks)
         line["gemm"] = bench_gemm(args, dev, peaks)
         line["moe"] = bench_moe(args, dev)
+        line["next_rows"] = bench_next_rows(args, dev, peaks)
         line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -541,6 +542,77 @@ def bench_gemm(args, dev, peaks):
         "gemm_then_quantize_c": chain,
         "data": "synthetic N(0,1) bf16 operands, both quantized with 4/6 (adaptive)",
     }
+
+
+def bench_next_rows(args, dev, peaks):
+    """SURVEY.md 8(f) rows 1-3, each timed like the headline (L2 flushed, CUDA
+    events, device busy while the host enqueues), bytes = algorithmic HBM
+    traffic: 2-D 16x16-tile weights (W and W^T containers from one read),
+    stochastic-rounding 4/6 quantize (numpy-Philox uniforms on the GPU), the
+    16-wide RHT (bf16 in, float64 out) and the fused selection statistics."""
+    import torch
+
+    import paper_2512_02010_b200 as f46
+
+    flush = L2Flush(dev)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, n=None):
+        n = n or max(5, args.steps)
+        fn()
+        ts = []
+        for i in range(n):
+            flush(i)
+            torch.cuda._sleep(200_000)
+            s, e = _events(2)
+            s.record(stream)
+            fn()
+            e.record(stream)
+            torch.cuda.synchronize()
+            ts.append(s.elapsed_time(e))
+        return sum(ts) / len(ts)
+
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(11)
+    W = (torch.randn(4096, 14336, generator=g, device=dev) * 0.02).to(torch.bfloat16)
+    cfg = f46.QuantConfig(scale_mode="adaptive")
+    ms = timed(lambda: f46.quantize_weights_2d(W, cfg, check_finite=False))
+    by = W.numel() * (2 * 2 + 2 * 0.5625)  # read twice (amax, quantize); W and W^T out
+    out["tile2d_4096x14336"] = {"ms": ms, "GB/s": by / ms / 1e6, "frac_of_hbm": by / ms / 1e6 / peaks["hbm_gbs"],
+                                "bytes_per_elem": 2 * 2 + 2 * 0.5625,
+                                "note": "amax + 2-D 16x16 4/6 tiles in exact float64, writes W and W^T"}
+    X = torch.randn(16384, 4096, generator=g, device=dev).to(torch.bfloat16)
+    sr = f46.QuantConfig(scale_mode="adaptive", rounding="sr", seed=3)
+    ms = timed(lambda: f46.quantize_tensor_adaptive(X, sr, sr_tag=2, check_finite=False))
+    by = X.numel() * BYTES_PER_ELEM
+    out["sr_16384x4096"] = {"ms": ms, "GB/s": by / ms / 1e6, "frac_of_hbm": by / ms / 1e6 / peaks["hbm_gbs"],
+                            "bytes_per_elem": BYTES_PER_ELEM,
+                            "note": "amax + 4/6 quantize with stochastic rounding (Philox4x64-10 per element)"}
+    spec = f46.RhtSpec(seed=3)
+    ms = timed(lambda: f46.apply_rht(X, spec))
+    by = X.numel() * (2 + 8)
+    out["rht16_16384x4096"] = {"ms": ms, "GB/s": by / ms / 1e6, "frac_of_hbm": by / ms / 1e6 / peaks["hbm_gbs"],
+                               "bytes_per_elem": 10, "note": "bf16 in, float64 out (numpy butterfly order)"}
+    from paper_2512_02010_b200 import _lib
+    from paper_2512_02010_b200.blockquant import amax_device
+
+    L = _lib.load()
+    nparts = 4 * torch.cuda.get_device_properties(dev).multi_processor_count
+    parts = torch.empty((nparts, 9), dtype=torch.float64, device=dev)
+
+    def stats():  # the device part of selection_stats (the fold to host syncs)
+        a = amax_device(X)
+        _lib.check(L.f46_selection_stats(X.data_ptr(), _lib.DT_BF16, X.shape[0], X.shape[1], 1536.0,
+                                         a.data_ptr(), 0.0, parts.data_ptr(), nparts, None,
+                                         stream.cuda_stream), "f46_selection_stats")
+
+    ms = timed(stats)
+    by = X.numel() * (2 + 2)
+    out["selection_stats_16384x4096"] = {"ms": ms, "GB/s": by / ms / 1e6,
+                                         "frac_of_hbm": by / ms / 1e6 / peaks["hbm_gbs"],
+                                         "bytes_per_elem": 4,
+                                         "note": "amax + one fused pass: both candidates' exact errors, 3 rules"}
+    return out
 
 
 def bench_moe(args, dev):

@@ -98,9 +98,8 @@ __device__ __forceinline__ float e4m3_to_f32(uint32_t code) {
 
 // FP4 magnitude of a 3-bit code m (0,.5,1,1.5,2,3,4,6), f32 exact.
 __device__ __forceinline__ float fp4_mag_f32(uint32_t m) {
-  const uint32_t e = m >> 1, mant = m & 1;
-  // e == 0: 0.5*mant; else (1 + 0.5*mant) * 2^(e-1)
-  return e == 0 ? 0.5f * (float)mant : (1.0f + 0.5f * (float)mant) * (float)(1u << (e - 1));
+  // twice the magnitudes {0, 1, 2, 3, 4, 6, 8, 12} as a byte table
+  return (float)(__byte_perm(0x03020100u, 0x0C080604u, m & 7u) & 0xFFu) * 0.5f;
 }
 
 // ----------------------------------------------------------------------------

@@ -709,6 +709,58 @@ __device__ __forceinline__ double pw_tile(const double* e) {
   return tot;
 }
 
+// The same 256-term pairwise sum with 16 lanes: lane 8h + j accumulates
+// r_j of half h (16 sequential adds), then the fixed tree
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and part0 + part1 through shuffles --
+// the identical association as pw_tile.  Every lane returns the total.
+__device__ __forceinline__ double pw_tile_par(const double* e, int lane) {
+  const int h = (lane >> 3) & 1, j = lane & 7;
+  double r = e[128 * h + j];
+#pragma unroll
+  for (int i = 8; i < 128; i += 8) r = __dadd_rn(r, e[128 * h + i + j]);
+  double t = __shfl_down_sync(0xFFFFFFFFu, r, 1);
+  const double a = __dadd_rn(r, t);  // meaningful in even j
+  t = __shfl_down_sync(0xFFFFFFFFu, a, 2);
+  const double b = __dadd_rn(a, t);  // meaningful in j % 4 == 0
+  t = __shfl_down_sync(0xFFFFFFFFu, b, 4);
+  const double c = __dadd_rn(b, t);  // part(h) in lane 8h
+  const double tot = __dadd_rn(c, __shfl_down_sync(0xFFFFFFFFu, c, 8));
+  return __shfl_sync(0xFFFFFFFFu, tot, 0);
+}
+
+// Exact FP4 codes of a lane's 8 tile values (float) under scale delta, from
+// the same proven bracket logic as the 1-D quantizer (f46_device.cuh):
+// tdir -1 / +1 pick one bound, 0 the split reciprocal, 2 resolves each
+// flagged nibble with the exact test through `load`.
+template <class Load>
+__device__ __forceinline__ uint32_t tile_codes8(const float (&xf)[8], float alpha, float delta,
+                                                int tdir, const Load& load) {
+  const float D = alpha * delta;
+  const float rq = rcp_approx(D) * F46_QLO;
+  float2 q[4];
+  if (tdir == 0) {
+    const float R = rcp_approx(D);
+    const float Rhi = __uint_as_float(__float_as_uint(R) & 0xFFFFFF00u);
+    const float Rlo = fmaf(-D, Rhi, 1.0f) * R;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      q[i] = make_float2(fmaf(xf[2 * i], Rlo, xf[2 * i] * Rhi), fmaf(xf[2 * i + 1], Rlo, xf[2 * i + 1] * Rhi));
+    return cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  }
+  const float r = tdir == 1 ? rq * F46_QHI_OVER_QLO : rq;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) q[i] = make_float2(xf[2 * i] * r, xf[2 * i + 1] * r);
+  uint32_t w = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+  if (tdir == 2) {
+    const float rh = rq * F46_QHI_OVER_QLO;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = make_float2(xf[2 * i] * rh, xf[2 * i + 1] * rh);
+    const uint32_t hi = cvt_e2m1x8(q[0], q[1], q[2], q[3]);
+    if (__builtin_expect((w ^ hi) != 0, 0)) w = fix_word(w, w ^ hi, 0, alpha, delta, load);
+  }
+  return w;
+}
+
 __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
   __shared__ double esq[8][256];
   __shared__ double eab[8][256];
@@ -728,6 +780,13 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
   const int64_t nbC = (p.C + 15) >> 4, nbR = (p.R + 15) >> 4;
   const int64_t kb4 = (nbC + 3) >> 2, kb4t = (nbR + 3) >> 2;
   const int tr_local = lane >> 1, tc_half = lane & 1;  // tile row, 8-column half
+  // Fast path (codes and scales from f32 brackets, proven exact; errors still
+  // float64): BF16/F32 input with a float32 alpha in range.  The rule only
+  // changes which float64 error sum decides, so it does not force the slow path.
+  const bool overridden = p.alpha_override > 0.0;
+  const TensorConsts tcs = make_consts(
+      alpha, RULE_MSE, p.dtype,
+      tie_direction(alpha, overridden ? 0.0 : *p.d_amax, p.mcap, p.dtype, overridden));
   double* es = esq[warp];
   double* ea = eab[warp];
   for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
@@ -736,36 +795,81 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
     double x[8];
     double tmax = 0.0;
     bool nf = false;
+    if (p.dtype == DT_F64) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      x[i] = q2_load(p, r, c0 + i);
-      nf |= !(fabs(x[i]) <= 1.7976931348623157e308);
-      tmax = fmax(tmax, fabs(x[i]));
+      for (int i = 0; i < 8; ++i) {
+        x[i] = q2_load(p, r, c0 + i);
+        nf |= !(fabs(x[i]) <= 1.7976931348623157e308);
+        tmax = fmax(tmax, fabs(x[i]));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xFFFFFFFFu, tmax, o));
+      nf = __any_sync(0xFFFFFFFFu, nf);
+    } else {
+      uint32_t mb = 0;  // |x| bit patterns order like the values (NaN above inf)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        x[i] = q2_load(p, r, c0 + i);
+        mb = max(mb, __float_as_uint((float)x[i]) & 0x7FFFFFFFu);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xFFFFFFFFu, mb, o));
+      nf = mb >= 0x7F800000u;
+      tmax = (double)__uint_as_float(mb);
     }
-    if (nf && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xFFFFFFFFu, tmax, o));
+    if (nf && p.d_flags && lane == 0) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
     uint32_t sc[2];
     uint32_t cw[2];  // 8 nibbles per candidate
     double err[2];
     const int ncand = p.mode == ADAPTIVE ? 2 : 1;
+    // fast-path scale codes (bmax = tile max, exact tie test); warp-uniform
+    const float tmaxf = (float)tmax;  // exact: BF16/F32 input
+    bool fast = p.dtype != DT_F64 && !tcs.force_exact &&
+                (__float_as_uint(tmaxf) - 0x2B800000u) < 0x28000000u;
+    uint32_t fsc[2] = {0, 0};
+    if (fast) {
+      for (int k = 0; k < ncand; ++k) {
+        const bool m4 = (p.mode == FIXED4 || k == 1);
+        fsc[k] = block_scale_code(tmaxf, tcs.alpha, m4 ? 4.f : 6.f, m4 ? tcs.r4_lo : tcs.r6_lo,
+                                  m4 ? tcs.r4_hi : tcs.r6_hi);
+        fast &= fsc[k] != 0u;  // an underflowed scale takes the float64 path
+      }
+    }
+    float xf[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) xf[i] = (float)x[i];
+    const auto gload = [&](int i) -> float { return (float)q2_load(p, r, c0 + i); };
     for (int k = 0; k < ncand; ++k) {
       const double m = (p.mode == FIXED4 || k == 1) ? 4.0 : 6.0;
-      uint32_t s = enc_e4m3_d(__ddiv_rn(tmax, __dmul_rn(alpha, m)));
-      if (tmax == 0.0) s = 1;
-      const double denom = __dmul_rn(alpha, dec_e4m3_d(s));
+      uint32_t s;
       uint32_t w = 0;
+      if (fast) {
+        s = fsc[k];
+        w = tile_codes8(xf, tcs.alpha, e4m3_to_f32(s), tcs.tdir, gload);
+      } else {
+        s = enc_e4m3_d(__ddiv_rn(tmax, __dmul_rn(alpha, m)));
+        if (tmax == 0.0) s = 1;
+      }
+      const double denom = __dmul_rn(alpha, dec_e4m3_d(s));
       double mx = 0.0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const double q = denom > 0.0 ? __ddiv_rn(x[i], denom)
-                                     : ((x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0);
-        const uint32_t code = enc_fp4_d(q);
-        w |= code << (4 * i);
+        uint32_t code;
+        if (fast) {
+          code = (w >> (4 * i)) & 0xFu;
+        } else {
+          const double q = denom > 0.0 ? __ddiv_rn(x[i], denom)
+                                       : ((x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0);
+          code = enc_fp4_d(q);
+          w |= code << (4 * i);
+        }
         const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(code), denom), x[i]);
-        es[tr_local * 16 + 8 * tc_half + i] = __dmul_rn(diff, diff);
-        ea[tr_local * 16 + 8 * tc_half + i] = fabs(diff);
-        mx = fmax(mx, fabs(diff));
+        if (p.rule == RULE_MSE)
+          es[tr_local * 16 + 8 * tc_half + i] = __dmul_rn(diff, diff);
+        else if (p.rule == RULE_L1)
+          ea[tr_local * 16 + 8 * tc_half + i] = fabs(diff);
+        else
+          mx = fmax(mx, fabs(diff));
       }
       __syncwarp();
       double e;
@@ -774,7 +878,7 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
         e = mx;
       } else {
-        e = __shfl_sync(0xFFFFFFFFu, lane == 0 ? pw_tile(p.rule == RULE_MSE ? es : ea) : 0.0, 0);
+        e = pw_tile_par(p.rule == RULE_MSE ? es : ea, lane);
       }
       __syncwarp();
       sc[k] = s;
@@ -799,31 +903,23 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
       }
     }
     if (p.codes_t) {
-      // W^T: tile row tr_local / column c of the tile -> W^T row (tc*16 + col),
-      // nibble position tr_local inside W^T's block tr.  Lane l gathers the
-      // 16 codes of W^T row tc*16 + l/2 ... through the warp.
+      // W^T: lane L builds W^T row tc*16 + L/2, word L%2 = tile rows
+      // 8(L%2)..+7 at tile column L/2.  Tile row i's codes of that column sit
+      // in lane 2i + (L/2 >= 8), nibble (L/2) % 8.
+      const int cc = lane >> 1, hw = lane & 1;
+      uint32_t wt = 0;
 #pragma unroll
-      for (int cc = 0; cc < 16; ++cc) {
-        // code of element (row tr_local, col cc): held by lane 2*tr_local + cc/8
-        const int src = 2 * (lane & 15) + (cc >> 3);
-        const uint32_t wv = __shfl_sync(0xFFFFFFFFu, w, src);
-        const uint32_t code = (wv >> (4 * (cc & 7))) & 0xFu;
-        // lanes 0..15 build W^T row (tc*16 + cc)'s nibble (lane) for lane < 16
-        const uint32_t part = code << (4 * ((lane & 15) & 7));
-        uint32_t acc = part;
-        // OR-reduce within groups of 8 lanes (lanes 0-7 -> low word, 8-15 -> high word)
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-        const int64_t rt = tc * 16 + cc;  // W^T row
-        if (lane < 16 && (lane & 7) == 0 && rt < p.C) {
-          const int64_t ct0 = tr * 16 + 8 * (lane >> 3);  // W^T columns of this word
-          uint32_t wt = acc;
-          if (ct0 + 8 > p.R) {
-            const int valid = (int)max((int64_t)0, p.R - ct0);
-            wt &= valid >= 8 ? 0xFFFFFFFFu : ((1u << (4 * valid)) - 1u);
-          }
-          reinterpret_cast<uint32_t*>(p.codes_t + rt * nbR * 8)[2 * tr + (lane >> 3)] = wt;
-        }
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t wv = __shfl_sync(0xFFFFFFFFu, w, 2 * (8 * hw + i) + (cc >> 3));
+        wt |= ((wv >> (4 * (cc & 7))) & 0xFu) << (4 * i);
+      }
+      const int64_t rt = tc * 16 + cc;        // W^T row
+      const int64_t ct0 = tr * 16 + 8 * hw;   // its first column in this word
+      if (rt < p.C && ct0 < p.R) {
+        if (ct0 + 8 > p.R) wt &= (1u << (4 * (int)(p.R - ct0))) - 1u;  // pad rows of W
+        reinterpret_cast<uint32_t*>(p.codes_t + rt * nbR * 8)[2 * tr + hw] = wt;
+      } else if (rt < p.C) {
+        reinterpret_cast<uint32_t*>(p.codes_t + rt * nbR * 8)[2 * tr + hw] = 0u;
       }
       if (p.scales_tc_t && lane < 16 && tc * 16 + lane < p.C)
         p.scales_tc_t[sf_tc_offset(tc * 16 + lane, tr, kb4t)] = (uint8_t)s;
