@@ -761,9 +761,12 @@ __device__ __forceinline__ uint32_t tile_codes8(const float (&xf)[8], float alph
   return w;
 }
 
-__global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
-  __shared__ double esq[8][256];
-  __shared__ double eab[8][256];
+#ifndef F46_Q2_MINB
+#define F46_Q2_MINB 4
+#endif
+__global__ void __launch_bounds__(256, F46_Q2_MINB) quant2d_kernel(Q2Params p) {
+  __shared__ double esq[8][256];   // the rule's per-element errors of one candidate
+  __shared__ double dtab[8][16];    // dequantized value of each code under the candidate
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t TR = (p.R + 15) >> 4, TC = (p.C + 15) >> 4;
   const int64_t ntiles = TR * TC;
@@ -788,7 +791,8 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
       alpha, RULE_MSE, p.dtype,
       tie_direction(alpha, overridden ? 0.0 : *p.d_amax, p.mcap, p.dtype, overridden));
   double* es = esq[warp];
-  double* ea = eab[warp];
+  double* ea = esq[warp];  // l1 and mse never both needed
+  double* dt = dtab[warp];
   for (int64_t tile = (int64_t)blockIdx.x * 8 + warp; tile < ntiles; tile += (int64_t)gridDim.x * 8) {
     const int64_t tr = tile / TC, tc = tile - tr * TC;
     const int64_t r = tr * 16 + tr_local, c0 = tc * 16 + 8 * tc_half;
@@ -807,11 +811,22 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
       nf = __any_sync(0xFFFFFFFFu, nf);
     } else {
       uint32_t mb = 0;  // |x| bit patterns order like the values (NaN above inf)
+      const int64_t e0 = r * p.C + c0;
+      if (p.dtype == DT_BF16 && r < p.R && c0 + 8 <= p.C && (e0 & 7) == 0 &&
+          (((uintptr_t)p.w) & 15) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.w) + e0));
+        const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        x[i] = q2_load(p, r, c0 + i);
-        mb = max(mb, __float_as_uint((float)x[i]) & 0x7FFFFFFFu);
+        for (int i = 0; i < 4; ++i) {
+          x[2 * i] = (double)__uint_as_float(wv[i] << 16);
+          x[2 * i + 1] = (double)__uint_as_float(wv[i] & 0xFFFF0000u);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = q2_load(p, r, c0 + i);
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mb = max(mb, __float_as_uint((float)x[i]) & 0x7FFFFFFFu);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mb = max(mb, __shfl_xor_sync(0xFFFFFFFFu, mb, o));
       nf = mb >= 0x7F800000u;
@@ -851,6 +866,10 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
         if (tmax == 0.0) s = 1;
       }
       const double denom = __dmul_rn(alpha, dec_e4m3_d(s));
+      // deq(code) = dec_fp4(code) * denom for the 16 codes (exact products)
+      __syncwarp();
+      if (lane < 16) dt[lane] = __dmul_rn(dec_fp4_d((uint32_t)lane), denom);
+      __syncwarp();
       double mx = 0.0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -863,7 +882,7 @@ __global__ void __launch_bounds__(256) quant2d_kernel(Q2Params p) {
           code = enc_fp4_d(q);
           w |= code << (4 * i);
         }
-        const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(code), denom), x[i]);
+        const double diff = __dsub_rn(dt[code], x[i]);
         if (p.rule == RULE_MSE)
           es[tr_local * 16 + 8 * tc_half + i] = __dmul_rn(diff, diff);
         else if (p.rule == RULE_L1)
@@ -1092,6 +1111,43 @@ __device__ __forceinline__ void exact_pass_sr(const double (&x)[16], double alph
   o.mx = mx;
 }
 
+// Fast, exact SR codes for one candidate (BF16/F32 input, f32 alpha, valid
+// scale).  The reference rounds q = RN64(x / denom) stochastically: inside
+// the grid interval [lo, hi) it takes the far end iff u < (|q| - lo) / gap
+// (positive) or u < (hi - |q|) / gap (negative); a - lo is exact (Sterbenz)
+// and gap is a power of two, so the only rounding is the quotient.  An f32
+// quotient (x * rcp(alpha*delta), relative error < 2^-21.9) gives the interval
+// position pt within 2^-20.4; when pt is 2^-18 clear of 0, 1 and u the
+// decision is the reference's, otherwise that element recomputes q in float64.
+__device__ __noinline__ uint32_t sr_code_exact(double xd, double denom, double u) {
+  return enc_fp4_sr_d(__ddiv_rn(xd, denom), u);
+}
+
+__device__ __forceinline__ uint32_t sr_code_fast(float x, float R, double u, double xd,
+                                                 double denom) {
+  if (x == 0.f) return signbit(x) ? 8u : 0u;
+  const float a = fabsf(x * R);
+  const uint32_t sgn = x < 0.f ? 8u : 0u;
+  if (a >= 6.0f * (1.0f + 0x1p-18f)) return 7u | sgn;  // saturates (exact q > 6 too)
+  // k = index of the grid point at or below a (0 .5 1 1.5 2 3 4 6): from the
+  // exponent and the top mantissa bit for a >= 1
+  const uint32_t b = __float_as_uint(a);
+  const int e = (int)(b >> 23) - 127;
+  const uint32_t k = a >= 1.0f ? (uint32_t)min(2 * e + 2 + (int)((b >> 22) & 1u), 7)
+                               : (a >= 0.5f ? 1u : 0u);
+  const float lo = fp4_mag_f32(k);
+  // 1 / gap: 2 2 2 2 1 1 0.5 for k = 0..6
+  const float inv_gap = k < 4 ? 2.0f : (k < 6 ? 1.0f : 0.5f);
+  const float pt = (a - lo) * inv_gap;
+  const float uf = (float)u;
+  if (k < 7 && pt > 0x1p-18f && pt < 1.0f - 0x1p-18f && fabsf(uf - (sgn ? 1.0f - pt : pt)) > 0x1p-18f) {
+    if (!sgn) return uf < pt ? k + 1 : k;
+    if (uf < 1.0f - pt) return k == 0 ? 0u : (8u | k);
+    return 8u | (k + 1);
+  }
+  return sr_code_exact(xd, denom, u);
+}
+
 struct SRParams {
   QParams q;
   uint64_t k6_0, k6_1, k4_0, k4_1;  // Philox keys of the m=6 / m=4 streams
@@ -1106,6 +1162,7 @@ __global__ void __launch_bounds__(128) quant_sr_kernel(SRParams sp) {
   const int64_t total = rows_pad * kb4 * 4;
   const double alpha = resolve_alpha(p);
   prologue_flags(p, alpha);
+  const TensorConsts tcs = make_consts(alpha, RULE_MSE, DT);
   bool nonfinite = false;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -1132,7 +1189,61 @@ __global__ void __launch_bounds__(128) quant_sr_kernel(SRParams sp) {
     const uint64_t blk = (uint64_t)(row * nb + kb);
     double u[16];
     BlockOut o;
-    if (p.mode == ADAPTIVE) {
+    // fast path: f32 brackets for the scale (exact tie test) and sr_code_fast
+    // for the codes; the float64 error sums and the decision are the reference's
+    double bmaxd = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bmaxd = fmax(bmaxd, fabs(xd[i]));
+    const float bmaxf = (float)bmaxd;
+    const bool fast = DT != DT_F64 && !tcs.force_exact && !(bmaxd > 3.4e38) &&
+                      (__float_as_uint(bmaxf) - 0x2B800000u) < 0x28000000u;
+    auto fast_pass = [&](float m, float r_lo, float r_hi, ExactPass& o2) -> bool {
+      const uint32_t sc = block_scale_code(bmaxf, tcs.alpha, m, r_lo, r_hi);
+      if (sc == 0) return false;
+      const float delta = e4m3_to_f32(sc);
+      const float R = rcp_approx(tcs.alpha * delta);
+      const double denom = (double)tcs.alpha * (double)delta;  // exact
+      double e[16];  // the rule's per-element error (squared / absolute)
+      double mx = 0.0;
+      uint64_t codes = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t c = sr_code_fast((float)xd[i], R, u[i], xd[i], denom);
+        codes |= (uint64_t)c << (4 * i);
+        const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(c), denom), xd[i]);
+        e[i] = p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff);
+        mx = fmax(mx, fabs(diff));
+      }
+      o2.codes = codes;
+      o2.sc = sc;
+      const double sum = p.rule == RULE_ABSMAX ? 0.0 : pw16(e);
+      o2.sq = sum;  // only the field rule_err reads for this rule is meaningful
+      o2.ab = sum;
+      o2.mx = mx;
+      return true;
+    };
+    if (fast && p.mode == ADAPTIVE) {
+      ExactPass p6, p4;
+      sr_uniforms16(blk, sp.k6_0, sp.k6_1, u);
+      bool ok = fast_pass(6.f, tcs.r6_lo, tcs.r6_hi, p6);
+      if (!ok) exact_pass_sr(xd, alpha, 6.0, u, p6);
+      sr_uniforms16(blk, sp.k4_0, sp.k4_1, u);
+      ok = fast_pass(4.f, tcs.r4_lo, tcs.r4_hi, p4);
+      if (!ok) exact_pass_sr(xd, alpha, 4.0, u, p4);
+      const bool k = rule_err(p4, p.rule) < rule_err(p6, p.rule);
+      o.codes = k ? p4.codes : p6.codes;
+      o.sc = k ? p4.sc : p6.sc;
+      o.pick4 = k;
+    } else if (fast) {
+      const bool four = p.mode == FIXED4;
+      ExactPass pp;
+      sr_uniforms16(blk, four ? sp.k4_0 : sp.k6_0, four ? sp.k4_1 : sp.k6_1, u);
+      if (!fast_pass(four ? 4.f : 6.f, four ? tcs.r4_lo : tcs.r6_lo, four ? tcs.r4_hi : tcs.r6_hi, pp))
+        exact_pass_sr(xd, alpha, four ? 4.0 : 6.0, u, pp);
+      o.codes = pp.codes;
+      o.sc = pp.sc;
+      o.pick4 = four;
+    } else if (p.mode == ADAPTIVE) {
       ExactPass p6, p4;
       sr_uniforms16(blk, sp.k6_0, sp.k6_1, u);
       exact_pass_sr(xd, alpha, 6.0, u, p6);

@@ -77,3 +77,19 @@ def test_sr_is_unbiased_in_expectation():
     err_rne = float((f46.dequantize_tensor(f46.quantize_tensor(x, f46.QuantConfig()), torch.float64)
                      - x.double()).abs().mean())
     assert err_sr < 0.5 * err_rne
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6"])
+def test_sr_fast_path_matches_float64_path(mode):
+    """BF16 input takes the f32-bracket SR path (sr_code_fast, float64 only
+    near a decision boundary); the same values as float64 input take the
+    float64 restatement everywhere.  2M elements, every code and scale equal."""
+    g = torch.Generator().manual_seed(17)
+    x = torch.randn(512, 4096, generator=g).to(torch.bfloat16)
+    cfg = f46.QuantConfig(scale_mode=mode, rounding="sr", seed=9)
+    fn = f46.quantize_tensor_adaptive if mode == "adaptive" else f46.quantize_tensor
+    a = fn(x.cuda(), cfg, sr_tag=1)
+    b = fn(x.double().cuda(), cfg, sr_tag=1)
+    assert a.alpha == b.alpha
+    assert torch.equal(a.scales_tc, b.scales_tc)
+    assert torch.equal(a.packed_codes, b.packed_codes)
