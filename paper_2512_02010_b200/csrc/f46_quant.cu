@@ -954,6 +954,27 @@ __global__ void __launch_bounds__(256, F46_Q2_MINB) quant2d_kernel(Q2Params p) {
 // squared error.  Each CTA writes 9 partials (6 counts, 3 sums) in a fixed
 // reduction order, so results are deterministic; the host folds the partials.
 // ---------------------------------------------------------------------------
+// exact_pass given the candidate's (exact) codes: the reference's float64
+// error terms and pairwise sums (blockquant.py:279, :283-293).
+__device__ __forceinline__ void exact_pass_codes(const double (&x)[16], uint64_t codes, double alpha,
+                                                 double delta, uint32_t sc, ExactPass& o) {
+  const double denom = __dmul_rn(alpha, delta);
+  double esq[16], eab[16];
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double diff = __dsub_rn(__dmul_rn(dec_fp4_d((uint32_t)(codes >> (4 * i)) & 15u), denom), x[i]);
+    esq[i] = __dmul_rn(diff, diff);
+    eab[i] = fabs(diff);
+    mx = fmax(mx, eab[i]);
+  }
+  o.codes = codes;
+  o.sc = sc;
+  o.sq = pw16(esq);
+  o.ab = pw16(eab);
+  o.mx = mx;
+}
+
 template <int DT>
 __global__ void __launch_bounds__(256) stats_kernel(const void* __restrict__ x, int64_t rows,
                                                     int64_t cols, double mcap, const double* d_amax,
@@ -967,6 +988,9 @@ __global__ void __launch_bounds__(256) stats_kernel(const void* __restrict__ x, 
     alpha = amax == 0.0 ? 1.0 : (double)((float)amax / (float)mcap);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && d_alpha_out) *d_alpha_out = alpha;
+  const bool overridden = alpha_override > 0.0;
+  const TensorConsts tcs = make_consts(
+      alpha, RULE_MSE, DT, tie_direction(alpha, overridden ? 0.0 : *d_amax, mcap, DT, overridden));
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < total;
        b += (int64_t)gridDim.x * blockDim.x) {
@@ -986,8 +1010,34 @@ __global__ void __launch_bounds__(256) stats_kernel(const void* __restrict__ x, 
         xd[i] = reinterpret_cast<const double*>(x)[row * cols + c];
     }
     ExactPass p6, p4;
-    exact_pass(xd, alpha, 6.0, p6);
-    exact_pass(xd, alpha, 4.0, p4);
+    // fast path: exact scale codes (f32 brackets + tie test) and exact codes
+    // (bracket logic), then the reference's float64 error terms
+    float2 xf[8];
+    float bmax = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      xf[q] = make_float2((float)xd[2 * q], (float)xd[2 * q + 1]);
+      bmax = fmax_nan(bmax, fmax_nan(fabsf(xf[q].x), fabsf(xf[q].y)));
+    }
+    bool fast = DT != DT_F64 && !tcs.force_exact &&
+                (__float_as_uint(bmax) - 0x2B800000u) < 0x28000000u;
+    uint32_t sc6 = 0, sc4 = 0;
+    if (fast) {
+      sc6 = block_scale_code(bmax, tcs.alpha, 6.f, tcs.r6_lo, tcs.r6_hi);
+      sc4 = block_scale_code(bmax, tcs.alpha, 4.f, tcs.r4_lo, tcs.r4_hi);
+      fast = sc6 != 0u && sc4 != 0u;
+    }
+    if (fast) {
+      const auto load = [&](int i) -> float { return (float)xd[i]; };
+      const float d6 = e4m3_to_f32(sc6), d4 = e4m3_to_f32(sc4);
+      const uint64_t c6 = exact_codes(xf, rcp_approx(tcs.alpha * d6) * F46_QLO, tcs.alpha, d6, tcs.tdir, load);
+      const uint64_t c4 = exact_codes(xf, rcp_approx(tcs.alpha * d4) * F46_QLO, tcs.alpha, d4, tcs.tdir, load);
+      exact_pass_codes(xd, c6, alpha, (double)d6, sc6, p6);
+      exact_pass_codes(xd, c4, alpha, (double)d4, sc4, p4);
+    } else {
+      exact_pass(xd, alpha, 6.0, p6);
+      exact_pass(xd, alpha, 4.0, p4);
+    }
     const bool k_sq = p4.sq < p6.sq, k_ab = p4.ab < p6.ab, k_mx = p4.mx < p6.mx;
     acc[0] += k_sq;
     acc[1] += k_ab;

@@ -71,3 +71,16 @@ def test_selection_stats_large_matches_quantize_pick4():
     assert st.fraction_4["mse"] == float(q.pick4.double().mean())
     mse = f46.reconstruction_mse(x, f46.dequantize_tensor(q, torch.float64))
     assert st.aggregate_mse["mse"] == pytest.approx(mse, rel=1e-12)
+
+
+def test_selection_stats_fast_path_matches_float64_path():
+    """BF16 input takes the f32-bracket codes, the same values as float64
+    input the float64 restatement: identical counts and sums."""
+    g = torch.Generator().manual_seed(23)
+    x = torch.randn(1024, 2048, generator=g).to(torch.bfloat16)
+    cfg = f46.QuantConfig(scale_mode="adaptive")
+    a = f46.selection_stats(x.cuda(), cfg)
+    b = f46.selection_stats(x.double().cuda(), cfg)
+    assert a.fraction_4 == b.fraction_4
+    assert a.disagreements == b.disagreements
+    assert a.aggregate_mse == b.aggregate_mse
