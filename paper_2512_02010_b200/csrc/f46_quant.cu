@@ -1331,17 +1331,25 @@ __global__ void __launch_bounds__(128) quant_sr_kernel(SRParams sp) {
 template <int DT>
 __global__ void __launch_bounds__(256) rht16_kernel(const void* __restrict__ x, int64_t ngroups,
                                                     double4 s0, double4 s1, double4 s2, double4 s3,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out, bool vec) {
   const double sg[16] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w,
                          s2.x, s2.y, s2.z, s2.w, s3.x, s3.y, s3.z, s3.w};
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
        g += (int64_t)gridDim.x * blockDim.x) {
     double a[16];
+    uint32_t wb[8];  // bf16: the group's 32 bytes in two 16-byte loads
+    if (DT == DT_BF16 && vec) {
+      const uint4* xv = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + g * 16);
+      const uint4 v0 = __ldg(xv), v1 = __ldg(xv + 1);
+      wb[0] = v0.x; wb[1] = v0.y; wb[2] = v0.z; wb[3] = v0.w;
+      wb[4] = v1.x; wb[5] = v1.y; wb[6] = v1.z; wb[7] = v1.w;
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       double v;
       if constexpr (DT == DT_BF16)
-        v = (double)__uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(x)[g * 16 + i] << 16);
+        v = vec ? (double)__uint_as_float((i & 1) ? (wb[i >> 1] & 0xFFFF0000u) : (wb[i >> 1] << 16))
+                : (double)__uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(x)[g * 16 + i] << 16);
       else if constexpr (DT == DT_F32)
         v = (double)reinterpret_cast<const float*>(x)[g * 16 + i];
       else
@@ -1361,8 +1369,15 @@ __global__ void __launch_bounds__(256) rht16_kernel(const void* __restrict__ x, 
 #pragma unroll
       for (int i = 0; i < 16; ++i) a[i] = b[i];
     }
+    // /4 == *0.25 exactly (power of two, both correctly rounded); 16-byte stores
+    if (vec) {
+      double2* o2 = reinterpret_cast<double2*>(out + g * 16);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) out[g * 16 + i] = __ddiv_rn(a[i], 4.0);
+      for (int i = 0; i < 8; ++i) o2[i] = make_double2(__dmul_rn(a[2 * i], 0.25), __dmul_rn(a[2 * i + 1], 0.25));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) out[g * 16 + i] = __dmul_rn(a[i], 0.25);
+    }
   }
 }
 
@@ -2388,15 +2403,16 @@ int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double
   int64_t grid = (ng + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;
+  const bool vec = ((((uintptr_t)x) | ((uintptr_t)out)) & 15) == 0;
   switch (dtype) {
     case F46_DT_BF16:
-      rht16_kernel<DT_BF16><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
+      rht16_kernel<DT_BF16><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out, vec);
       break;
     case F46_DT_F32:
-      rht16_kernel<DT_F32><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
+      rht16_kernel<DT_F32><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out, vec);
       break;
     case F46_DT_F64:
-      rht16_kernel<DT_F64><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out);
+      rht16_kernel<DT_F64><<<(unsigned)grid, 256, 0, s>>>(x, ng, s0, s1, s2, s3, out, vec);
       break;
     default:
       return F46_ERR_INVALID_ARG;

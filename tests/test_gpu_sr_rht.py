@@ -93,3 +93,16 @@ def test_sr_fast_path_matches_float64_path(mode):
     assert a.alpha == b.alpha
     assert torch.equal(a.scales_tc, b.scales_tc)
     assert torch.equal(a.packed_codes, b.packed_codes)
+
+
+def test_rht_bf16_vector_path_matches_float64_input():
+    """The BF16 kernel (16-byte loads / stores) and the float64-input kernel
+    compute the same float64 butterflies: identical outputs, also unaligned."""
+    g = torch.Generator().manual_seed(4)
+    x = torch.randn(256, 1024, generator=g).to(torch.bfloat16).cuda()
+    spec = f46.RhtSpec(seed=6)
+    a = f46.apply_rht(x, spec)
+    b = f46.apply_rht(x.double(), spec)
+    assert torch.equal(a, b)
+    xs = x.reshape(-1)[16:16 + 4096]  # 32-byte offset view: still 16-byte aligned
+    assert torch.equal(f46.apply_rht(xs, spec), f46.apply_rht(xs.double(), spec))
