@@ -1326,6 +1326,171 @@ __global__ void __launch_bounds__(128) quant_sr_kernel(SRParams sp) {
   if (nonfinite && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
 }
 
+// One block entirely in float64 (the reference's restatement), by one thread:
+// the SR quad kernel's fallback for blocks outside the f32 fast path.
+template <int DT>
+__device__ __noinline__ void sr_block_exact(const SRParams sp, double alpha, int64_t row, int64_t kb,
+                                            int64_t nb, int64_t kb4) {
+  const QParams& p = sp.q;
+  double xd[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int64_t c = kb * 16 + i;
+    if (c >= p.cols)
+      xd[i] = 0.0;
+    else if constexpr (DT == DT_BF16)
+      xd[i] = (double)__uint_as_float((uint32_t)(reinterpret_cast<const uint16_t*>(p.x)[row * p.cols + c]) << 16);
+    else
+      xd[i] = (double)reinterpret_cast<const float*>(p.x)[row * p.cols + c];
+  }
+  const uint64_t blk = (uint64_t)(row * nb + kb);
+  double u[16];
+  BlockOut o;
+  if (p.mode == ADAPTIVE) {
+    ExactPass p6, p4;
+    sr_uniforms16(blk, sp.k6_0, sp.k6_1, u);
+    exact_pass_sr(xd, alpha, 6.0, u, p6);
+    sr_uniforms16(blk, sp.k4_0, sp.k4_1, u);
+    exact_pass_sr(xd, alpha, 4.0, u, p4);
+    const bool k = rule_err(p4, p.rule) < rule_err(p6, p.rule);
+    o.codes = k ? p4.codes : p6.codes;
+    o.sc = k ? p4.sc : p6.sc;
+    o.pick4 = k;
+  } else {
+    const bool four = p.mode == FIXED4;
+    ExactPass pp;
+    sr_uniforms16(blk, four ? sp.k4_0 : sp.k6_0, four ? sp.k4_1 : sp.k6_1, u);
+    exact_pass_sr(xd, alpha, four ? 4.0 : 6.0, u, pp);
+    o.codes = pp.codes;
+    o.sc = pp.sc;
+    o.pick4 = four;
+  }
+  uint64_t codes = o.codes;
+  const int64_t c0 = kb * 16;
+  if (c0 + 16 > p.cols) codes &= ((1ull << (4 * (int)(p.cols - c0))) - 1);
+  *reinterpret_cast<uint64_t*>(p.codes + blk * 8) = codes;
+  p.scales_tc[sf_tc_offset(row, kb, kb4)] = (uint8_t)o.sc;
+  if (p.scales_rm) p.scales_rm[blk] = (uint8_t)o.sc;
+  if (p.pick4) p.pick4[blk] = (uint8_t)o.pick4;
+}
+
+// SR quantize with four threads per block (BF16 / F32 input): thread t of a
+// quad owns elements 4t..4t+3, which are exactly the four uniforms of Philox
+// counter 4b + t + 1, so each thread runs one Philox call per candidate.  The
+// block max, the rule's error sum (numpy's pw16 association: r_j = e_j +
+// e_{j+8} from the thread two lanes up, then ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) across the pair) and the decision go through quad
+// shuffles.  Blocks outside the f32 fast path (alpha override that is not a
+// float32, extreme magnitudes, underflowed scale) fall back to sr_block_exact.
+template <int DT>
+__global__ void __launch_bounds__(256, 3) quant_sr4_kernel(SRParams sp) {
+  const QParams& p = sp.q;
+  const int64_t nb = (p.cols + 15) >> 4;
+  const int64_t kb4 = (nb + 3) >> 2;
+  const int64_t rows_pad = (p.rows + 127) & ~(int64_t)127;
+  const int64_t total = rows_pad * kb4 * 4;
+  const double alpha = resolve_alpha(p);
+  prologue_flags(p, alpha);
+  const TensorConsts tcs = make_consts(alpha, RULE_MSE, DT);
+  const int lane = threadIdx.x & 31, t = lane & 3, qbase = lane & ~3;
+  const unsigned FULL = 0xFFFFFFFFu;
+  bool nonfinite = false;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; base < total;
+       base += nwarps * 8) {
+    const int64_t idx = base + (lane >> 2);
+    const int64_t row = idx / (kb4 * 4), kb = idx - row * (kb4 * 4);
+    const bool inb = idx < total;
+    const bool active = inb && row < p.rows && kb < nb;
+    if (inb && !active && t == 0) p.scales_tc[sf_tc_offset(row, kb, kb4)] = 0;  // layout padding
+    // the thread's four values (pads and inactive lanes: +0)
+    float xf[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t c = kb * 16 + 4 * t + i;
+      float v = 0.f;
+      if (active && c < p.cols) {
+        if constexpr (DT == DT_BF16)
+          v = __uint_as_float((uint32_t)(reinterpret_cast<const uint16_t*>(p.x)[row * p.cols + c]) << 16);
+        else
+          v = reinterpret_cast<const float*>(p.x)[row * p.cols + c];
+      }
+      xf[i] = v;
+    }
+    uint32_t mb = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mb = max(mb, __float_as_uint(xf[i]) & 0x7FFFFFFFu);
+    mb = max(mb, __shfl_xor_sync(FULL, mb, 1));
+    mb = max(mb, __shfl_xor_sync(FULL, mb, 2));
+    nonfinite |= active && mb >= 0x7F800000u;
+    const float bmax = __uint_as_float(mb);
+    bool fast = !tcs.force_exact && (mb - 0x2B800000u) < 0x28000000u;
+    const bool two = p.mode == ADAPTIVE;
+    const bool m4only = p.mode == FIXED4;
+    uint32_t sc[2] = {0, 0};
+    double err[2] = {0.0, 0.0};
+    uint32_t cw[2] = {0, 0};  // the thread's 4 codes per candidate
+    if (fast) {
+      sc[0] = block_scale_code(bmax, tcs.alpha, m4only ? 4.f : 6.f, m4only ? tcs.r4_lo : tcs.r6_lo,
+                               m4only ? tcs.r4_hi : tcs.r6_hi);
+      if (two) sc[1] = block_scale_code(bmax, tcs.alpha, 4.f, tcs.r4_lo, tcs.r4_hi);
+      fast = sc[0] != 0u && (!two || sc[1] != 0u);
+    }
+    if (!fast) sc[0] = sc[1] = 0x38;  // placeholders: every lane runs the shuffles below
+    {
+      const uint64_t blk = (uint64_t)(row * nb + kb);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (k == 1 && !two) break;
+        const bool use4 = (k == 1) || m4only;
+        uint64_t c4[4] = {4 * blk + (uint64_t)t + 1, 0, 0, 0};
+        philox4x64_10(c4, use4 ? sp.k4_0 : sp.k6_0, use4 ? sp.k4_1 : sp.k6_1);
+        const float delta = e4m3_to_f32(sc[k]);
+        const float R = rcp_approx(tcs.alpha * delta);
+        const double denom = (double)tcs.alpha * (double)delta;  // exact
+        double e[4];
+        double mx = 0.0;
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double u = (double)(c4[i] >> 11) * 0x1p-53;
+          const uint32_t c = sr_code_fast(xf[i], R, u, (double)xf[i], denom);
+          w |= c << (4 * i);
+          const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(c), denom), (double)xf[i]);
+          e[i] = p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff);
+          mx = fmax(mx, fabs(diff));
+        }
+        double tot;
+        if (p.rule == RULE_ABSMAX) {
+          mx = fmax(mx, __shfl_xor_sync(FULL, mx, 1));
+          tot = fmax(mx, __shfl_xor_sync(FULL, mx, 2));
+        } else {
+          double r[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) r[i] = __dadd_rn(e[i], __shfl_down_sync(FULL, e[i], 2));
+          const double a = __dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3]));
+          tot = __shfl_sync(FULL, __dadd_rn(a, __shfl_down_sync(FULL, a, 1)), qbase);
+        }
+        err[k] = tot;
+        cw[k] = w;
+      }
+      const bool k4 = two ? (err[1] < err[0]) : m4only;
+      const int ki = (two && k4) ? 1 : 0;
+      if (active && fast) {
+        reinterpret_cast<uint16_t*>(p.codes + (row * nb + kb) * 8)[t] = (uint16_t)cw[ki];
+        if (t == 0) {
+          p.scales_tc[sf_tc_offset(row, kb, kb4)] = (uint8_t)sc[ki];
+          if (p.scales_rm) p.scales_rm[row * nb + kb] = (uint8_t)sc[ki];
+          if (p.pick4) p.pick4[row * nb + kb] = (uint8_t)k4;
+        }
+      }
+    }
+    if (!fast && active && t == 0) sr_block_exact<DT>(sp, alpha, row, kb, nb, kb4);
+  }
+  nonfinite = __any_sync(FULL, nonfinite);
+  if (nonfinite && lane == 0 && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+}
+
 // transforms.py:92-97 apply_rht: y = fwht(g * signs) / sqrt(16) per group of
 // 16 along the last dim, float64, numpy's butterfly order (h = 1, 2, 4, 8).
 template <int DT>
@@ -2375,12 +2540,22 @@ int f46_quantize_sr(const void* x, int dtype, int64_t rows, int64_t cols, int mo
   int64_t grid = (total + 127) / 128;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
+  const bool quad = !getenv("F46_SR_ONE_THREAD");
+  int64_t grid4 = (total * 4 + 255) / 256;
+  const int64_t cap4 = (int64_t)num_sms() * 8;
+  if (grid4 > cap4) grid4 = cap4;
   switch (dtype) {
     case F46_DT_BF16:
-      quant_sr_kernel<DT_BF16><<<(unsigned)grid, 128, 0, s>>>(sp);
+      if (quad)
+        quant_sr4_kernel<DT_BF16><<<(unsigned)grid4, 256, 0, s>>>(sp);
+      else
+        quant_sr_kernel<DT_BF16><<<(unsigned)grid, 128, 0, s>>>(sp);
       break;
     case F46_DT_F32:
-      quant_sr_kernel<DT_F32><<<(unsigned)grid, 128, 0, s>>>(sp);
+      if (quad)
+        quant_sr4_kernel<DT_F32><<<(unsigned)grid4, 256, 0, s>>>(sp);
+      else
+        quant_sr_kernel<DT_F32><<<(unsigned)grid, 128, 0, s>>>(sp);
       break;
     case F46_DT_F64:
       quant_sr_kernel<DT_F64><<<(unsigned)grid, 128, 0, s>>>(sp);
