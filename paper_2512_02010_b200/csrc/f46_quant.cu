@@ -2595,8 +2595,11 @@ int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double
   return launch_status();
 }
 
+#define F46_STR2(x) #x
+#define F46_STR(x) F46_STR2(x)
 const char* f46_build_info(void) {
-  return "fouroversix sm_100a (tcgen05/TMA) built with nvcc " __VERSION__;
+  return "fouroversix sm_100a (tcgen05/TMA) built with nvcc " F46_STR(__CUDACC_VER_MAJOR__) "." F46_STR(
+      __CUDACC_VER_MINOR__) "." F46_STR(__CUDACC_VER_BUILD__) ", host compiler " __VERSION__;
 }
 
 }  // extern "C"
