@@ -946,6 +946,229 @@ __global__ void __launch_bounds__(256, F46_Q2_MINB) quant2d_kernel(Q2Params p) {
   }
 }
 
+// 2-D tiles, version 2: two tiles per warp, 16 lanes per tile.  Lane (h, j)
+// (h = row half, j = 0..7) owns tile columns j and 8+j of rows 8h..8h+7, which
+// are exactly the 16 terms of the reference's pairwise accumulator r_j of half
+// h (p = 16*row + col, r_j = e[128h + j] + e[128h + 8 + j] + e[128h + 16 + j]
+// + ..., transforms.py:125-130): each lane sums its errors in registers in
+// that order, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and part0 + part1 go
+// through shuffles -- no shared memory.  Its two columns are also two W^T
+// words directly; the row-major W words are gathered with shuffles.  Codes and
+// scales come from the f32 bracket logic (exact, as in K2), errors in float64.
+// Tiles the fast path cannot take (all-zero excepted) use quant2d_tile_exact.
+__device__ __noinline__ void quant2d_tile_exact(const Q2Params p, double alpha, int64_t tr, int64_t tc) {
+  const int64_t nbC = (p.C + 15) >> 4, nbR = (p.R + 15) >> 4;
+  const int64_t kb4 = (nbC + 3) >> 2, kb4t = (nbR + 3) >> 2;
+  double x[256];
+  double tmax = 0.0;
+  for (int i = 0; i < 256; ++i) {
+    x[i] = q2_load(p, tr * 16 + (i >> 4), tc * 16 + (i & 15));
+    tmax = fmax(tmax, fabs(x[i]));
+  }
+  uint8_t code[2][256];
+  uint32_t sc[2];
+  double err[2];
+  const int ncand = p.mode == ADAPTIVE ? 2 : 1;
+  for (int k = 0; k < ncand; ++k) {
+    const double m = (p.mode == FIXED4 || k == 1) ? 4.0 : 6.0;
+    uint32_t s = enc_e4m3_d(__ddiv_rn(tmax, __dmul_rn(alpha, m)));
+    if (tmax == 0.0) s = 1;
+    const double denom = __dmul_rn(alpha, dec_e4m3_d(s));
+    double e[256];
+    double mx = 0.0;
+    for (int i = 0; i < 256; ++i) {
+      const double q = denom > 0.0 ? __ddiv_rn(x[i], denom) : ((x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0);
+      code[k][i] = (uint8_t)enc_fp4_d(q);
+      const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(code[k][i]), denom), x[i]);
+      e[i] = p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff);
+      mx = fmax(mx, fabs(diff));
+    }
+    sc[k] = s;
+    err[k] = p.rule == RULE_ABSMAX ? mx : pw_tile(e);
+  }
+  const bool k4 = (p.mode == ADAPTIVE) ? (err[1] < err[0]) : (p.mode == FIXED4);
+  const int ki = (p.mode == ADAPTIVE && k4) ? 1 : 0;
+  for (int rr = 0; rr < 16; ++rr) {
+    const int64_t r = tr * 16 + rr;
+    if (r < p.R) {
+      uint64_t w = 0;
+      for (int c = 0; c < 16; ++c)
+        if (tc * 16 + c < p.C) w |= (uint64_t)code[ki][16 * rr + c] << (4 * c);
+      *reinterpret_cast<uint64_t*>(p.codes + (r * nbC + tc) * 8) = w;
+      p.scales_tc[sf_tc_offset(r, tc, kb4)] = (uint8_t)sc[ki];
+      if (p.scales_rm) p.scales_rm[r * nbC + tc] = (uint8_t)sc[ki];
+      if (p.pick4) p.pick4[r * nbC + tc] = (uint8_t)k4;
+    }
+    const int64_t rt = tc * 16 + rr;  // W^T row = W column
+    if (p.codes_t && rt < p.C) {
+      uint64_t w = 0;
+      for (int c = 0; c < 16; ++c)
+        if (tr * 16 + c < p.R) w |= (uint64_t)code[ki][16 * c + rr] << (4 * c);
+      *reinterpret_cast<uint64_t*>(p.codes_t + (rt * nbR + tr) * 8) = w;
+      p.scales_tc_t[sf_tc_offset(rt, tr, kb4t)] = (uint8_t)sc[ki];
+    }
+  }
+}
+
+#ifndef F46_Q2V2_MINB
+#define F46_Q2V2_MINB 4
+#endif
+__global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params p) {
+  const int lane = threadIdx.x & 31, hw = lane >> 4, l = lane & 15, h = l >> 3, j = l & 7;
+  const int hbase = lane & 16;
+  const unsigned FULL = 0xFFFFFFFFu;
+  const int64_t TR = (p.R + 15) >> 4, TC = (p.C + 15) >> 4;
+  const int64_t ntiles = TR * TC;
+  double alpha = p.alpha_override;
+  if (!(alpha > 0.0)) {
+    const double amax = *p.d_amax;
+    alpha = amax == 0.0 ? 1.0 : (double)((float)amax / (float)p.mcap);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (p.d_alpha_out) *p.d_alpha_out = alpha;
+    if (p.alpha_override <= 0.0 && p.d_flags && !(*p.d_amax <= 1.7976931348623157e308))
+      atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+  }
+  const int64_t nbC = (p.C + 15) >> 4, nbR = (p.R + 15) >> 4;
+  const int64_t kb4 = (nbC + 3) >> 2, kb4t = (nbR + 3) >> 2;
+  const bool overridden = p.alpha_override > 0.0;
+  const TensorConsts tcs = make_consts(
+      alpha, RULE_MSE, p.dtype,
+      tie_direction(alpha, overridden ? 0.0 : *p.d_amax, p.mcap, p.dtype, overridden));
+  const int64_t G = (int64_t)gridDim.x * (blockDim.x >> 5) * 2;
+  bool nonfinite = false;
+  for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2; t0 < ntiles;
+       t0 += G) {
+    const int64_t tile = t0 + hw;
+    const bool live = tile < ntiles;
+    const int64_t tr = live ? tile / TC : 0, tc = live ? tile - tr * TC : 0;
+    const int64_t r0 = tr * 16 + 8 * h, c0 = tc * 16;
+    // the lane's 16 values in accumulation order: (row r0 + i/2, col (i%2)*8 + j)
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t r = r0 + (i >> 1), c = c0 + ((i & 1) << 3) + j;
+      x[i] = live ? (float)q2_load(p, r, c) : 0.f;
+    }
+    uint32_t mb = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mb = max(mb, __float_as_uint(x[i]) & 0x7FFFFFFFu);
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) mb = max(mb, __shfl_xor_sync(FULL, mb, o));
+    nonfinite |= live && mb >= 0x7F800000u;
+    const float tmax = __uint_as_float(mb);
+    const bool zero = mb == 0u;
+    bool fast = !tcs.force_exact && (mb - 0x2B800000u) < 0x28000000u;
+    const int ncand = p.mode == ADAPTIVE ? 2 : 1;
+    uint32_t sc[2] = {1u, 1u};
+    if (fast) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (k < ncand) {
+          const bool m4 = (p.mode == FIXED4 || k == 1);
+          sc[k] = block_scale_code(tmax, tcs.alpha, m4 ? 4.f : 6.f, m4 ? tcs.r4_lo : tcs.r6_lo,
+                                   m4 ? tcs.r4_hi : tcs.r6_hi);
+          fast &= sc[k] != 0u;
+        }
+      }
+    }
+    if (!fast) sc[0] = sc[1] = 0x38;  // placeholders: every lane runs the shuffles below
+    float2 x2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x2[q] = make_float2(x[2 * q], x[2 * q + 1]);
+    const auto gload = [&](int i) -> float {
+      return (float)q2_load(p, r0 + (i >> 1), c0 + ((i & 1) << 3) + j);
+    };
+    uint64_t cw[2] = {0, 0};
+    double err[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (k >= ncand) break;
+      const float delta = e4m3_to_f32(sc[k]);
+      const uint64_t codes =
+          exact_codes(x2, rcp_approx(tcs.alpha * delta) * F46_QLO, tcs.alpha, delta, tcs.tdir, gload);
+      const double denom = (double)tcs.alpha * (double)delta;  // exact
+      double r = 0.0, mx = 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double diff = __dsub_rn(__dmul_rn(dec_fp4_d((uint32_t)(codes >> (4 * i)) & 15u), denom),
+                                      (double)x[i]);
+        const double e = p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff);
+        r = i == 0 ? e : __dadd_rn(r, e);
+        mx = fmax(mx, fabs(diff));
+      }
+      double tot;
+      if (p.rule == RULE_ABSMAX) {
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        tot = mx;
+      } else {
+        const double a = __dadd_rn(r, __shfl_down_sync(FULL, r, 1));   // j even
+        const double b = __dadd_rn(a, __shfl_down_sync(FULL, a, 2));   // j % 4 == 0
+        const double c = __dadd_rn(b, __shfl_down_sync(FULL, b, 4));   // j == 0: part(h)
+        const double t = __dadd_rn(c, __shfl_down_sync(FULL, c, 8));   // lane (0, 0)
+        tot = __shfl_sync(FULL, t, hbase);
+      }
+      cw[k] = codes;
+      err[k] = tot;
+    }
+    const bool k4 = (p.mode == ADAPTIVE) ? (err[1] < err[0]) : (p.mode == FIXED4);
+    const int ki = (p.mode == ADAPTIVE && k4) ? 1 : 0;
+    uint64_t codes = cw[ki];
+    uint32_t s = sc[ki];
+    if (zero) {
+      // all-zero tile (blockquant.py:241): scale code 1, codes keep -0.0's sign, tie keeps 6
+      codes = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) codes |= (uint64_t)(__float_as_uint(x[i]) >> 31) << (4 * i + 3);
+      s = 1;
+    }
+    const bool ok = fast || zero;
+    // W rows: lane (h, j) writes row r0 + j; column c's nibble comes from lane
+    // (h, c % 8), element 2j + c / 8
+    uint64_t wrow = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t lo = __shfl_sync(FULL, (uint32_t)codes, hbase + 8 * h + c);
+      const uint32_t hi = __shfl_sync(FULL, (uint32_t)(codes >> 32), hbase + 8 * h + c);
+      const uint64_t src = ((uint64_t)hi << 32) | lo;
+      wrow |= ((src >> (8 * j)) & 0xFull) << (4 * c);            // element 2j: column c
+      wrow |= ((src >> (8 * j + 4)) & 0xFull) << (4 * (c + 8));  // element 2j + 1: column 8 + c
+    }
+    if (live && ok) {
+      const int64_t r = r0 + j;
+      if (r < p.R) {
+        uint64_t w = wrow;
+        if (c0 + 16 > p.C) w &= (1ull << (4 * (int)(p.C - c0))) - 1;  // pad columns
+        *reinterpret_cast<uint64_t*>(p.codes + (r * nbC + tc) * 8) = w;
+        p.scales_tc[sf_tc_offset(r, tc, kb4)] = (uint8_t)s;
+        if (p.scales_rm) p.scales_rm[r * nbC + tc] = (uint8_t)s;
+        if (p.pick4) p.pick4[r * nbC + tc] = (uint8_t)(zero ? (p.mode == FIXED4) : k4);
+      }
+      if (p.codes_t) {
+        // W^T rows c0 + j (even elements) and c0 + 8 + j (odd elements), word h
+#pragma unroll
+        for (int par = 0; par < 2; ++par) {
+          uint32_t wt = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) wt |= (uint32_t)((codes >> (4 * (2 * i + par))) & 0xFull) << (4 * i);
+          const int64_t rt = c0 + 8 * par + j;
+          if (rt < p.C && r0 < p.R) {
+            if (r0 + 8 > p.R) wt &= (1u << (4 * (int)(p.R - r0))) - 1u;  // pad rows of W
+            reinterpret_cast<uint32_t*>(p.codes_t + (rt * nbR + tr) * 8)[h] = wt;
+            if (h == 0) p.scales_tc_t[sf_tc_offset(rt, tr, kb4t)] = (uint8_t)s;
+          } else if (rt < p.C) {
+            reinterpret_cast<uint32_t*>(p.codes_t + (rt * nbR + tr) * 8)[h] = 0u;
+          }
+        }
+      }
+    }
+    if (live && !ok && l == 0) quant2d_tile_exact(p, alpha, tr, tc);
+  }
+  nonfinite = __any_sync(FULL, nonfinite);
+  if (nonfinite && lane == 0 && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
+}
+
 // ---------------------------------------------------------------------------
 // Selection statistics for all three rules in one pass (adaptive.py:159-187):
 // per block both candidates' exact float64 errors (sq / abs / max, numpy
@@ -2493,7 +2716,15 @@ int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, in
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  quant2d_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
+  if (dtype != F46_DT_F64 && !getenv("F46_Q2_V1")) {
+    int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
+    const int64_t cap2 = (int64_t)num_sms() * 8;
+    if (g2 > cap2) g2 = cap2;
+    if (g2 < 1) g2 = 1;
+    quant2d_v2_kernel<<<(unsigned)g2, 256, 0, s>>>(p);
+  } else {
+    quant2d_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
+  }
   return launch_status();
 }
 

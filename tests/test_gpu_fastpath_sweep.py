@@ -88,3 +88,25 @@ def test_dequant_routes_agree(shape, dtype):
         # one rounding of the float64 value (torch's f64 -> bf16 goes through f32)
         from tests.test_gpu_quant import f64_to_bf16_bits
         assert np.array_equal(d.view(torch.int16).numpy().view(np.uint16), f64_to_bf16_bits(d64))
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6", "fixed4"])
+def test_tile2d_v2_special_tiles_equal_v1(mode, monkeypatch):
+    """The two-tiles-per-warp 2-D kernel against the one-tile-per-warp kernel
+    on all-zero tiles (with -0.0), tiles beyond the fast path's magnitude
+    range (float32 input, 1e30) and ragged edges."""
+    g = torch.Generator().manual_seed(8)
+    x = torch.randn(70, 90, generator=g) * 0.02
+    x[:16, :16] = 0.0
+    x[0:16:3, 0:16:5] = -0.0
+    x[16:32, 32:48] *= 1e32          # tile max ~1e30: float64 tile path
+    x[48:64, 16:32] = 1e-30          # tiny tile
+    for t in (x.float(), x.to(torch.bfloat16)):
+        cfg = f46.QuantConfig(scale_mode=mode)
+        a = f46.quantize_weights_2d(t.cuda(), cfg, want_rowmajor=True)
+        monkeypatch.setenv("F46_Q2_V1", "1")
+        b = f46.quantize_weights_2d(t.cuda(), cfg, want_rowmajor=True)
+        monkeypatch.delenv("F46_Q2_V1")
+        same(a, b)
+        same(a.transposed, b.transposed)
+        assert torch.equal(a.scales_rm, b.scales_rm)
