@@ -37,6 +37,12 @@
 #ifndef F46_PRMT_LO
 #define F46_PRMT_LO 0
 #endif
+#ifndef F46_AMGM
+#define F46_AMGM 1
+#endif
+#ifndef F46_T0SPLIT
+#define F46_T0SPLIT 0
+#endif
 #ifndef F46_NEWTON
 #define F46_NEWTON 0
 #endif
@@ -294,6 +300,7 @@ struct TensorConsts {
   // -1 keep the lower code, +1 take the upper code, 0 ties-to-even,
   // 2 unknown -> exact per-element test.
   int tdir;
+  uint32_t zero;  // 0, but not a compile-time constant (unpack_e2m1x8)
 };
 
 // For BF16 input whose alpha was computed from amax A (no override), every
@@ -329,6 +336,7 @@ __device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, in
   t.tdir = tdir;
   t.alpha_d = alpha_d;
   t.alpha = (float)alpha_d;
+  t.zero = __float_as_uint(t.alpha) >> 31;  // alpha > 0
   const bool f32_exact = ((double)t.alpha == alpha_d);
   t.force_exact = !(f32_exact && alpha_d >= 0x1p-50 && alpha_d <= 0x1p50) ||
                   rule != RULE_MSE || dtype == DT_F64;
@@ -689,6 +697,134 @@ __device__ __forceinline__ bool block_sl(const float2 (&x)[8], float bmax, const
     out.sc = k ? (pl >> 8) : (pl & 0xFFu);
     out.pick4 = k;
   }
+  return ok;
+}
+
+// ----------------------------------------------------------------------------
+// Candidate pass that keeps its codes (adaptive, BF16, known tie direction)
+// ----------------------------------------------------------------------------
+
+// The 8 E2M1 codes of one packed word -> four f16x2 values (exact).  ptxas
+// reads each byte with the unpack's byte selector (F2FP.F16.E2M1.UNPACK_B
+// Rw.B1/.B2/.B3), so no byte extraction is emitted -- but only when `w` is
+// opaque to it: if ptxas can see that w was assembled from cvt bytes
+// (cvt_e2m1x8) it forwards the bytes and, under 12.9, reads bytes 2 and 3 of
+// the 4-way .b8 split from RZ.  Callers therefore pass w ^ z with z a runtime
+// zero (one LOP3 per word).
+__device__ __forceinline__ void unpack_e2m1x8(uint32_t w, uint32_t (&v)[4]) {
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
+      "mov.b32 {b0, b1, b2, b3}, %4;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %0, b0;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %1, b1;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %2, b2;\n\t"
+      "cvt.rn.f16x2.e2m1x2 %3, b3;\n\t}"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+      : "r"(w));
+}
+
+// One candidate of one block: codes of q = x*rq packed into two words (the
+// F2FP merge chain builds each word without byte shuffles) and decoded back
+// from the words, and the quotient-space error  sum_i (v_i - q_i)^2  (f32x2
+// accumulator, as cand_err).  The codes are those of the quotient q itself, so
+// when rq is the bound that the tensor's tie direction makes exact (lower
+// bound for TDIR -1, upper bound for +1) they are the reference's codes and the
+// stored candidate needs no second pass.
+template <bool SPLIT = false>
+__device__ __forceinline__ float cand_codes(const float2 (&x)[8], float rq, uint32_t z,
+                                            uint32_t& w0, uint32_t& w1, float rlo = 0.f) {
+  const float2 r2 = make_float2(rq, rq);
+  float2 q[8];
+  if constexpr (SPLIT) {
+    // rq = Rhi (16 significant bits), rlo = Rlo: q = fma(x, Rlo, x*Rhi) (codes_split)
+    const float2 l2 = make_float2(rlo, rlo);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q[p] = __ffma2_rn(x[p], l2, __fmul2_rn(x[p], r2));
+  } else {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
+  }
+  w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]) ^ z;  // z == 0 (see unpack_e2m1x8)
+  w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]) ^ z;
+  uint32_t v[8];
+  unpack_e2m1x8(w0, *reinterpret_cast<uint32_t(*)[4]>(&v[0]));
+  unpack_e2m1x8(w1, *reinterpret_cast<uint32_t(*)[4]>(&v[4]));
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const float2 r = make_float2(fhadd_h<0>(v[p], -q[p].x), fhadd_h<1>(v[p], -q[p].y));
+    acc = __ffma2_rn(r, r, acc);
+  }
+  return acc.x + acc.y;
+}
+
+// Adaptive block, BF16 input, computed alpha (TDIR -1, 0 or +1): block_sl with
+// the candidates' codes kept.  TDIR -1 / +1: the candidate pass runs on the
+// lower / upper bound quotient, whose codes are exact (tie_direction()), so
+// the winner's codes are a select.  TDIR 0: the pass runs on the lower bound;
+// only the winner's upper-bound codes are formed, and a nibble where the two
+// differ is an exact tie (exact_codes's tdir 0 rule picks the even code).  The
+// upper-bound quotient is within 2^-19.5 of the exact one, inside the 2^-15
+// decision tolerance's margin (the lower bound's 2^-19.9 gives 2^-16.4 of it).
+template <int TDIR>
+__device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const TensorConsts& tc,
+                                        BlockOut& out) {
+  const uint32_t bb = __float_as_uint(bmax);
+  bool ok = (bb - 0x2B800000u) < 0x28000000u;  // bmax in [2^-40, 2^40)
+  const float alpha = tc.alpha;
+  const float2 b2 = make_float2(bmax, bmax);
+  const float2 th = __fmul2_rn(b2, make_float2(tc.r6_hi, tc.r4_hi));
+  const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
+  const uint32_t ph = cvt_e4m3x2(th.y, th.x), pl = cvt_e4m3x2(tl.y, tl.x);
+  ok &= (ph == pl) & ((pl & 0xFFu) != 0u);
+  uint32_t dd;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(dd) : "h"((uint16_t)pl));
+  const float2 dlt = make_float2(fhadd_h<0>(dd, -0.f), fhadd_h<1>(dd, -0.f));
+  const float2 D = __fmul2_rn(make_float2(alpha, alpha), dlt);
+  float2 rq = __fmul2_rn(make_float2(rcp_approx(D.x), rcp_approx(D.y)),
+                         make_float2(F46_QLO, F46_QLO));
+  if constexpr (TDIR == 1) rq = __fmul2_rn(rq, make_float2(F46_QHI_OVER_QLO, F46_QHI_OVER_QLO));
+  uint32_t a0, a1, b0, b1;  // M=6 and M=4 code words
+#if F46_T0SPLIT
+  float2 sq;
+  if constexpr (TDIR == 0) {
+    // exact quotients (codes_split): D is exact, the candidate codes are the
+    // reference's, and x is dead after the two passes
+    const float2 R = make_float2(rcp_approx(D.x), rcp_approx(D.y));
+    const float2 Rhi = make_float2(__uint_as_float(__float_as_uint(R.x) & 0xFFFFFF00u),
+                                   __uint_as_float(__float_as_uint(R.y) & 0xFFFFFF00u));
+    const float2 Rlo = __fmul2_rn(__ffma2_rn(make_float2(-D.x, -D.y), Rhi, make_float2(1.f, 1.f)), R);
+    sq = make_float2(cand_codes<true>(x, Rhi.x, tc.zero, a0, a1, Rlo.x),
+                     cand_codes<true>(x, Rhi.y, tc.zero, b0, b1, Rlo.y));
+  } else {
+    sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));
+  }
+#else
+  const float2 sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));
+#endif
+  const float2 s = __fmul2_rn(sq, __fmul2_rn(D, D));
+  const float ssum = s.x + s.y;
+#if F46_AMGM
+  // block_sl's tolerance with its square root bounded by AM-GM:
+  // 2^-15 bmax sqrt(ssum) <= 2^-18 bmax^2 + 2^-14 ssum, so
+  // tol <= (2^-14 + 2^-14) ssum + (2^-18 + 2^-32) bmax^2 + 2^-140.
+  const float tol = fmaf(0x1.002p-13f, ssum, fmaf(0x1.002p-18f * bmax, bmax, 0x1p-140f));
+#else
+  const float tol = fmaf(0x1p-15f * bmax, sqrt_approx(ssum),
+                         fmaf(0x1p-14f, ssum, fmaf(0x1p-32f * bmax, bmax, 0x1p-140f)));
+#endif
+  ok &= fabsf(s.x - s.y) > tol;  // NaN (from a rejected block) compares false
+  const bool k = s.y < s.x;
+  uint32_t w0 = k ? b0 : a0, w1 = k ? b1 : a1;
+  if constexpr (TDIR == 0 && !F46_T0SPLIT) {
+    const float rh = (k ? rq.y : rq.x) * F46_QHI_OVER_QLO;
+    const uint64_t hi = codes_of(x, rh);
+    const uint32_t d0 = w0 ^ (uint32_t)hi, d1 = w1 ^ (uint32_t)(hi >> 32);
+    w0 += (d0 & 0x22222222u) >> 1;
+    w1 += (d1 & 0x22222222u) >> 1;
+  }
+  out.codes = ((uint64_t)w1 << 32) | w0;
+  out.sc = k ? (pl >> 8) : (pl & 0xFFu);
+  out.pick4 = k;
   return ok;
 }
 

@@ -207,6 +207,12 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_MINB
 #define F46_MINB 4
 #endif
+#ifndef F46_FULL
+#define F46_FULL 1
+#endif
+#ifndef F46_V3
+#define F46_V3 1
+#endif
 #ifndef F46_UNCOND_STORE
 #define F46_UNCOND_STORE 1
 #endif
@@ -432,7 +438,11 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 #if F46_UNCOND_STORE
         // straight line: store unconditionally; a deferred block's bytes are
         // rewritten by the resolve pass (ordered after this by __syncwarp)
-        const bool ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
+        bool ok;
+        if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
+          ok = block46<TDIR>(x, bmax, tc, o);
+        else
+          ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
         *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
         p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
         if constexpr (EXTRA) {
@@ -496,6 +506,97 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
   }
 }
 
+// The streaming loop for whole segments (cols % kSegElems == 0, no parity
+// views): tile t is bytes [t, t+1) * kTileBytes of the input, its blocks are
+// t*kSegBlocks + [0, kSegBlocks), so every cursor is a multiple of t.  All
+// per-tile bookkeeping is warp-uniform (the warp index comes through a shuffle,
+// so the compiler keeps it in uniform registers and the bulk copy needs no
+// per-lane election loop).
+template <int DT, int MODE, int TDIR>
+__device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
+                                            uint64_t* wb, uint32_t* dl, uint32_t t_begin,
+                                            uint32_t t_end, uint32_t n_seg) {
+  constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
+  constexpr uint32_t kTileBytes = kSegElems * kEsz;
+  constexpr uint32_t kSegBlocks = kSegElems / 16;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nb = (uint32_t)p.cols >> 4;
+  const uint32_t kb4 = (nb + 3) >> 2;
+  const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s)
+      if (t_begin + s < t_end) {
+        mbar_expect_tx(&wb[s], kTileBytes);
+        bulk_load(wsm + s * kTileBytes, xb + (size_t)(t_begin + s) * kTileBytes, kTileBytes, &wb[s]);
+      }
+  }
+  uint32_t row = t_begin / n_seg, seg = t_begin - row * n_seg;
+  auto sf_row = [&](uint32_t r) -> uint32_t {  // lane's scale byte for block 0 of row r
+    return ((r >> 7) * kb4 + (lane >> 2)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (lane & 3);
+  };
+  uint32_t srow = sf_row(row);
+  uint8_t* cptr = p.codes + (size_t)t_begin * (kSegBlocks * 8) + lane * 8;
+  const ExactArgs ea{p.x, p.codes, p.scales_tc, nullptr, nullptr, p.cols, MODE, p.rule};
+  int s = 0;
+  uint32_t parity = 0, ndefer = 0;
+  for (uint32_t t = t_begin; t < t_end; ++t) {
+    mbar_wait(&wb[s], parity);
+    const uint32_t blk0 = wsm + s * kTileBytes + lane * (16 * kEsz);
+    const uint32_t soff = srow + seg * (kSegBlocks / 4) * 512;
+    uint32_t fails = 0;
+#pragma unroll
+    for (int j = 0; j < kBPL; ++j) {
+      const uint32_t blk_addr = blk0 + j * (32 * 16 * kEsz);
+      float2 x[8];
+      float bmax;
+      load_block<DT>(blk_addr, x, bmax);
+      BlockOut o;
+      bool ok;
+      if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
+        ok = block46<TDIR>(x, bmax, tc, o);
+      else
+        ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
+      *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
+      p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
+      fails |= (ok ? 0u : 1u) << j;
+    }
+    if (__builtin_expect(__any_sync(0xFFFFFFFFu, fails != 0), 0)) {
+      const uint32_t rbk = t * kSegBlocks;
+#pragma unroll
+      for (int j = 0; j < kBPL; ++j) {
+        const bool f = (fails >> j) & 1u;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, f);
+        if (f) dl[ndefer + __popc(m & ((1u << lane) - 1))] = rbk + lane + 32 * j;
+        ndefer += __popc(m);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && t + kStages < t_end) {
+      mbar_expect_tx(&wb[s], kTileBytes);
+      bulk_load(wsm + s * kTileBytes, xb + (size_t)(t + kStages) * kTileBytes, kTileBytes, &wb[s]);
+    }
+    if (++s == kStages) {
+      s = 0;
+      parity ^= 1u;
+    }
+    cptr += kSegBlocks * 8;
+    if (++seg == n_seg) {
+      seg = 0;
+      ++row;
+      srow = sf_row(row);
+    }
+    // deferred blocks: exact path, outside the hot loop's straight line
+    if (__builtin_expect(ndefer > kDefer - kSegBlocks, 0)) {
+      for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
+      __syncwarp();
+      ndefer = 0;
+    }
+  }
+  __syncwarp();
+  for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
+}
+
 template <int DT, int MODE, bool EXTRA>
 __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParams p) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
@@ -504,11 +605,13 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   __shared__ __align__(8) uint64_t bars[kWarps][kStages];
   __shared__ uint32_t defer[kWarps][kDefer];
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: the compiler then knows it is warp-uniform
+  const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t cols = (uint32_t)p.cols;
   const uint32_t nb = cols >> 4;
   const uint32_t kb4 = (nb + 3) >> 2;
   const uint32_t n_seg = (cols + kSegElems - 1) / kSegElems;
+  const bool full = !EXTRA && (cols % kSegElems) == 0;
   const uint32_t total = (uint32_t)p.rows * n_seg;
   const uint32_t gw = blockIdx.x * kWarps + warp, G = gridDim.x * kWarps;
 
@@ -538,6 +641,24 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
     const uint32_t nblk = (uint32_t)p.rows * nb;
     for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
       exact_block_global<DT>(ea, alpha_d, b, kb4, p.d_flags);
+  } else if (full && F46_FULL) {
+    if constexpr (DT == DT_BF16) {
+      switch (tc.tdir) {
+        case -1:
+          stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          break;
+        case 0:
+          stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          break;
+        case 1:
+          stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          break;
+        default:
+          stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+      }
+    } else {
+      stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+    }
   } else if constexpr (DT == DT_BF16) {
     switch (tc.tdir) {
       case -1:

@@ -207,3 +207,41 @@ def test_k2_multi_launch_row_slabs(mode, monkeypatch):
     assert torch.equal(got.packed_codes, ref.packed_codes)
     assert torch.equal(got.scales_tc, ref.scales_tc)
     assert torch.equal(got.pick4, ref.pick4) and torch.equal(got.scales_rm, ref.scales_rm)
+
+
+def tie_direction(amax: float, mcap: float) -> int:
+    """Sign of RN32(amax/mcap)*mcap - amax (f46_device.cuh tie_direction):
+    -1 when alpha rounds up, +1 when it rounds down, 0 when it is exact."""
+    a = float(np.float32(np.float32(amax) / np.float32(mcap)))
+    d = a * mcap - amax
+    return -1 if d > 0 else (1 if d < 0 else 0)
+
+
+# amax values whose alpha = RN32(amax / 1536) is exact (0), rounded up (-1) or
+# rounded down (+1); the streaming kernel is specialised on that direction.
+TIE_AMAX = [6.0, 7.5, 5.25, 5.75, 5.3125, 6.5, 7.0, 5.1875]
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6", "fixed4"])
+@pytest.mark.parametrize("amax", TIE_AMAX)
+def test_timed_instantiation_every_tie_direction(mode, amax):
+    """The instantiation bench.py times (no row-major scales, no pick4 output,
+    whole 2048-element segments) against the oracle, bit for bit, for tensors
+    of every tensor-wide tie direction (TDIR -1, 0, +1): packed codes and
+    tcgen05-layout scales."""
+    x = bf16_randn((512, 4096), int(amax * 64), std=0.5)
+    x[7, 100] = amax
+    x[300, 5] = -amax
+    q = f46.quantize_tensor_adaptive(x.cuda(), f46.QuantConfig(scale_mode="adaptive")) \
+        if mode == "adaptive" else f46.quantize_tensor(x.cuda(), f46.QuantConfig(scale_mode=mode))
+    ref = O.quantize(bits(x), mode)
+    assert q.alpha == ref["alpha"]
+    got = q.packed_codes.cpu().numpy()
+    bad = np.argwhere(got != ref["codes"])
+    assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[:4].tolist()}"
+    sc = f46.blockquant.tc_to_rowmajor(q.scales_tc, 512, 256).cpu().numpy()
+    assert np.array_equal(sc, ref["scales"].reshape(512, -1))
+
+
+def test_tie_amax_cover_every_direction():
+    assert {tie_direction(a, 1536.0) for a in TIE_AMAX} == {-1, 0, 1}

@@ -11,7 +11,7 @@ mode = os.environ.get("MODE", "adaptive")
 dt = os.environ.get("DT", "bf16")
 L = _lib.load()
 dev = torch.device("cuda")
-g = torch.Generator(device=dev).manual_seed(1234)
+g = torch.Generator(device=dev).manual_seed(int(os.environ.get("SEED", 1234)))
 x = torch.randn(rows, cols, generator=g, device=dev)
 x = x.to(torch.bfloat16) if dt == "bf16" else x
 codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=dev)

@@ -50,7 +50,13 @@ for i in range(25):
     if i >= 5:
         ta.append(a.elapsed_time(b))
 ma = sum(ta) / len(ta)
+am = float(amax.item())
+al = float(torch.tensor(am, dtype=torch.float32) / torch.tensor(mcap, dtype=torch.float32))
+tdir = "-1" if al * mcap > am else ("+1" if al * mcap < am else "0")
+print(f"seed {os.environ.get('SEED', 1234)} tdir {tdir} ", end="")
 print(f"{os.path.basename(os.environ.get('F46_LIB_PATH', 'default'))} {mode} {dt}: K2 {ms*1e3:.1f} us  {rows*cols*bpe/ms/1e6:.0f} GB/s | K1 amax {ma*1e3:.1f} us {rows*cols*(bpe-0.5625)/ma/1e6:.0f} GB/s")
+if os.environ.get("NODQ"):
+    sys.exit(0)
 # K3 dequantize of the same tensor (bf16 and f32 out)
 alpha = torch.tensor([0.003], dtype=torch.float64, device=dev)
 for od, dtc, ob in ((torch.bfloat16, _lib.DT_BF16, 2), (torch.float32, _lib.DT_F32, 4)):
