@@ -37,11 +37,8 @@
 #ifndef F46_PRMT_LO
 #define F46_PRMT_LO 0
 #endif
-#ifndef F46_AMGM
-#define F46_AMGM 1
-#endif
-#ifndef F46_T0SPLIT
-#define F46_T0SPLIT 0
+#ifndef F46_TAB
+#define F46_TAB 1
 #endif
 #ifndef F46_NEWTON
 #define F46_NEWTON 0
@@ -729,20 +726,12 @@ __device__ __forceinline__ void unpack_e2m1x8(uint32_t w, uint32_t (&v)[4]) {
 // when rq is the bound that the tensor's tie direction makes exact (lower
 // bound for TDIR -1, upper bound for +1) they are the reference's codes and the
 // stored candidate needs no second pass.
-template <bool SPLIT = false>
 __device__ __forceinline__ float cand_codes(const float2 (&x)[8], float rq, uint32_t z,
-                                            uint32_t& w0, uint32_t& w1, float rlo = 0.f) {
+                                            uint32_t& w0, uint32_t& w1) {
   const float2 r2 = make_float2(rq, rq);
   float2 q[8];
-  if constexpr (SPLIT) {
-    // rq = Rhi (16 significant bits), rlo = Rlo: q = fma(x, Rlo, x*Rhi) (codes_split)
-    const float2 l2 = make_float2(rlo, rlo);
 #pragma unroll
-    for (int p = 0; p < 8; ++p) q[p] = __ffma2_rn(x[p], l2, __fmul2_rn(x[p], r2));
-  } else {
-#pragma unroll
-    for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
-  }
+  for (int p = 0; p < 8; ++p) q[p] = __fmul2_rn(x[p], r2);
   w0 = cvt_e2m1x8(q[0], q[1], q[2], q[3]) ^ z;  // z == 0 (see unpack_e2m1x8)
   w1 = cvt_e2m1x8(q[4], q[5], q[6], q[7]) ^ z;
   uint32_t v[8];
@@ -765,65 +754,84 @@ __device__ __forceinline__ float cand_codes(const float2 (&x)[8], float rq, uint
 // differ is an exact tie (exact_codes's tdir 0 rule picks the even code).  The
 // upper-bound quotient is within 2^-19.5 of the exact one, inside the 2^-15
 // decision tolerance's margin (the lower bound's 2^-19.9 gives 2^-16.4 of it).
+// Per-tensor table of everything block46 derives from a scale code c
+// (0..127): {rq, rh, D*D, c} with D = RN(alpha * E4M3(c)), rq = RN(rcp(D) * QLO),
+// rh = RN(rq * QHI_OVER_QLO) -- the same roundings block_sl performs per block.
+// Code 0 (an underflowed scale) maps to NaN, which fails the decision test.
+__device__ __forceinline__ float4 scale_entry(uint32_t c, float alpha) {
+  const float D = alpha * e4m3_to_f32(c);
+  const float rq = rcp_approx(D) * F46_QLO;
+  float4 e = make_float4(rq, rq * F46_QHI_OVER_QLO, D * D, __uint_as_float(c));
+  if (c == 0) e.x = e.y = e.z = __uint_as_float(0x7FC00000u);
+  return e;
+}
+
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+
+// Adaptive block, BF16 input, computed alpha (TDIR -1, 0 or +1): block_sl with
+// the candidates' codes kept.  TDIR -1 / +1: the candidate pass runs on the
+// lower / upper bound quotient, whose codes are exact (tie_direction()), so
+// the winner's codes are a select.  TDIR 0: the pass runs on the lower bound;
+// only the winner's upper-bound codes are formed, and a nibble where the two
+// differ is an exact tie whose even code is kept (exact_codes' tdir 0 rule).
+// The upper-bound quotient is within 2^-19.5 of the exact one, inside the 2^-15
+// decision tolerance's margin (the lower bound's 2^-19.9 gives 2^-16.4 of it).
+// The per-code reciprocals come from the shared table `tab` (scale_entry).
 template <int TDIR>
 __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const TensorConsts& tc,
-                                        BlockOut& out) {
+                                        uint32_t tab, BlockOut& out) {
   const uint32_t bb = __float_as_uint(bmax);
   bool ok = (bb - 0x2B800000u) < 0x28000000u;  // bmax in [2^-40, 2^40)
-  const float alpha = tc.alpha;
   const float2 b2 = make_float2(bmax, bmax);
   const float2 th = __fmul2_rn(b2, make_float2(tc.r6_hi, tc.r4_hi));
   const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
   const uint32_t ph = cvt_e4m3x2(th.y, th.x), pl = cvt_e4m3x2(tl.y, tl.x);
-  ok &= (ph == pl) & ((pl & 0xFFu) != 0u);
+  ok &= (ph == pl);
+#if F46_TAB
+  const float4 e6 = lds_f4(tab + ((pl << 4) & 0xFF0u));
+  const float4 e4 = lds_f4(tab + ((pl >> 4) & 0xFF0u));
+#else
+  // the same entries computed in place (packed over the two candidates)
+  ok &= (pl & 0xFFu) != 0u;
   uint32_t dd;
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(dd) : "h"((uint16_t)pl));
   const float2 dlt = make_float2(fhadd_h<0>(dd, -0.f), fhadd_h<1>(dd, -0.f));
-  const float2 D = __fmul2_rn(make_float2(alpha, alpha), dlt);
-  float2 rq = __fmul2_rn(make_float2(rcp_approx(D.x), rcp_approx(D.y)),
-                         make_float2(F46_QLO, F46_QLO));
-  if constexpr (TDIR == 1) rq = __fmul2_rn(rq, make_float2(F46_QHI_OVER_QLO, F46_QHI_OVER_QLO));
-  uint32_t a0, a1, b0, b1;  // M=6 and M=4 code words
-#if F46_T0SPLIT
-  float2 sq;
-  if constexpr (TDIR == 0) {
-    // exact quotients (codes_split): D is exact, the candidate codes are the
-    // reference's, and x is dead after the two passes
-    const float2 R = make_float2(rcp_approx(D.x), rcp_approx(D.y));
-    const float2 Rhi = make_float2(__uint_as_float(__float_as_uint(R.x) & 0xFFFFFF00u),
-                                   __uint_as_float(__float_as_uint(R.y) & 0xFFFFFF00u));
-    const float2 Rlo = __fmul2_rn(__ffma2_rn(make_float2(-D.x, -D.y), Rhi, make_float2(1.f, 1.f)), R);
-    sq = make_float2(cand_codes<true>(x, Rhi.x, tc.zero, a0, a1, Rlo.x),
-                     cand_codes<true>(x, Rhi.y, tc.zero, b0, b1, Rlo.y));
-  } else {
-    sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));
-  }
-#else
-  const float2 sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));
+  const float2 D = __fmul2_rn(make_float2(tc.alpha, tc.alpha), dlt);
+  const float2 rq2 = __fmul2_rn(make_float2(rcp_approx(D.x), rcp_approx(D.y)),
+                                make_float2(F46_QLO, F46_QLO));
+  const float2 rh2 = TDIR >= 0 ? __fmul2_rn(rq2, make_float2(F46_QHI_OVER_QLO, F46_QHI_OVER_QLO)) : rq2;
+  const float2 DD = __fmul2_rn(D, D);
+  const float4 e6 = make_float4(rq2.x, rh2.x, DD.x, __uint_as_float(pl & 0xFFu));
+  const float4 e4 = make_float4(rq2.y, rh2.y, DD.y, __uint_as_float(pl >> 8));
 #endif
-  const float2 s = __fmul2_rn(sq, __fmul2_rn(D, D));
+  const float2 rq = TDIR == 1 ? make_float2(e6.y, e4.y) : make_float2(e6.x, e4.x);
+  uint32_t a0, a1, b0, b1;  // M=6 and M=4 code words
+  const float2 sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));
+  const float2 s = __fmul2_rn(sq, make_float2(e6.z, e4.z));
   const float ssum = s.x + s.y;
-#if F46_AMGM
   // block_sl's tolerance with its square root bounded by AM-GM:
   // 2^-15 bmax sqrt(ssum) <= 2^-18 bmax^2 + 2^-14 ssum, so
   // tol <= (2^-14 + 2^-14) ssum + (2^-18 + 2^-32) bmax^2 + 2^-140.
   const float tol = fmaf(0x1.002p-13f, ssum, fmaf(0x1.002p-18f * bmax, bmax, 0x1p-140f));
-#else
-  const float tol = fmaf(0x1p-15f * bmax, sqrt_approx(ssum),
-                         fmaf(0x1p-14f, ssum, fmaf(0x1p-32f * bmax, bmax, 0x1p-140f)));
-#endif
-  ok &= fabsf(s.x - s.y) > tol;  // NaN (from a rejected block) compares false
+  ok &= fabsf(s.x - s.y) > tol;  // NaN (underflowed scale, rejected block) compares false
   const bool k = s.y < s.x;
   uint32_t w0 = k ? b0 : a0, w1 = k ? b1 : a1;
-  if constexpr (TDIR == 0 && !F46_T0SPLIT) {
-    const float rh = (k ? rq.y : rq.x) * F46_QHI_OVER_QLO;
-    const uint64_t hi = codes_of(x, rh);
-    const uint32_t d0 = w0 ^ (uint32_t)hi, d1 = w1 ^ (uint32_t)(hi >> 32);
-    w0 += (d0 & 0x22222222u) >> 1;
-    w1 += (d1 & 0x22222222u) >> 1;
+  if constexpr (TDIR == 0) {
+    const uint64_t hi = codes_of(x, k ? e4.y : e6.y);
+    // nibbles where the bounds disagree are exact ties: keep the even code
+    // (the lower code when it is even, else the upper one)
+    const uint32_t m0 = (w0 & 0x11111111u) * 15u, m1 = (w1 & 0x11111111u) * 15u;
+    w0 ^= (w0 ^ (uint32_t)hi) & m0;
+    w1 ^= (w1 ^ (uint32_t)(hi >> 32)) & m1;
   }
   out.codes = ((uint64_t)w1 << 32) | w0;
-  out.sc = k ? (pl >> 8) : (pl & 0xFFu);
+  out.sc = __float_as_uint(k ? e4.w : e6.w);
   out.pick4 = k;
   return ok;
 }

@@ -26,6 +26,7 @@
 #include <stdio.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/fouroversix.h"
 #include "f46_device.cuh"
@@ -210,6 +211,9 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_FULL
 #define F46_FULL 1
 #endif
+#ifndef F46_STEP2
+#define F46_STEP2 0
+#endif
 #ifndef F46_V3
 #define F46_V3 1
 #endif
@@ -366,7 +370,7 @@ constexpr int kDefer = 2 * kSegElems / 16;  // deferred-block slots per warp (a 
 template <int DT, int MODE, bool EXTRA, int TDIR>
 __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                            uint64_t* wb, uint32_t* dl, uint32_t t_begin,
-                                           uint32_t t_end) {
+                                           uint32_t t_end, uint32_t tab) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
   constexpr int kTileBytes = kSegElems * kEsz;
   constexpr uint32_t kSegBlocks = kSegElems / 16;
@@ -440,7 +444,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         // rewritten by the resolve pass (ordered after this by __syncwarp)
         bool ok;
         if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
-          ok = block46<TDIR>(x, bmax, tc, o);
+          ok = block46<TDIR>(x, bmax, tc, tab, o);
         else
           ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
         *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
@@ -515,7 +519,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 template <int DT, int MODE, int TDIR>
 __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                             uint64_t* wb, uint32_t* dl, uint32_t t_begin,
-                                            uint32_t t_end, uint32_t n_seg) {
+                                            uint32_t t_end, uint32_t n_seg, uint32_t tab) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
   constexpr uint32_t kTileBytes = kSegElems * kEsz;
   constexpr uint32_t kSegBlocks = kSegElems / 16;
@@ -538,11 +542,19 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
   uint32_t srow = sf_row(row);
   uint8_t* cptr = p.codes + (size_t)t_begin * (kSegBlocks * 8) + lane * 8;
   const ExactArgs ea{p.x, p.codes, p.scales_tc, nullptr, nullptr, p.cols, MODE, p.rule};
-  int s = 0;
   uint32_t parity = 0, ndefer = 0;
-  for (uint32_t t = t_begin; t < t_end; ++t) {
-    mbar_wait(&wb[s], parity);
-    const uint32_t blk0 = wsm + s * kTileBytes + lane * (16 * kEsz);
+  uint32_t t = t_begin;
+  // one tile from stage S (a compile-time constant: barrier and buffer
+  // addresses fold); returns false when the warp's range is done
+  auto step = [&](auto S_) -> bool {
+#if F46_STEP2
+    constexpr int S = decltype(S_)::value;
+#else
+    const int S = S_;
+#endif
+    if (t >= t_end) return false;
+    mbar_wait(&wb[S], parity);
+    const uint32_t blk0 = wsm + S * kTileBytes + lane * (16 * kEsz);
     const uint32_t soff = srow + seg * (kSegBlocks / 4) * 512;
     uint32_t fails = 0;
 #pragma unroll
@@ -554,7 +566,7 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
       BlockOut o;
       bool ok;
       if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
-        ok = block46<TDIR>(x, bmax, tc, o);
+        ok = block46<TDIR>(x, bmax, tc, tab, o);
       else
         ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
       *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
@@ -570,29 +582,34 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
         if (f) dl[ndefer + __popc(m & ((1u << lane) - 1))] = rbk + lane + 32 * j;
         ndefer += __popc(m);
       }
+      // deferred blocks: exact path, once the list is half full
+      if (ndefer > kDefer - kSegBlocks) {
+        __syncwarp();
+        for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
+        ndefer = 0;
+      }
     }
     __syncwarp();
     if (lane == 0 && t + kStages < t_end) {
-      mbar_expect_tx(&wb[s], kTileBytes);
-      bulk_load(wsm + s * kTileBytes, xb + (size_t)(t + kStages) * kTileBytes, kTileBytes, &wb[s]);
+      mbar_expect_tx(&wb[S], kTileBytes);
+      bulk_load(wsm + S * kTileBytes, xb + (size_t)(t + kStages) * kTileBytes, kTileBytes, &wb[S]);
     }
-    if (++s == kStages) {
-      s = 0;
-      parity ^= 1u;
-    }
+    ++t;
     cptr += kSegBlocks * 8;
     if (++seg == n_seg) {
       seg = 0;
       ++row;
       srow = sf_row(row);
     }
-    // deferred blocks: exact path, outside the hot loop's straight line
-    if (__builtin_expect(ndefer > kDefer - kSegBlocks, 0)) {
-      for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
-      __syncwarp();
-      ndefer = 0;
-    }
-  }
+    return true;
+  };
+  static_assert(kStages == 2, "stream_full unrolls two stages");
+#if F46_STEP2
+  while (step(std::integral_constant<int, 0>{}) && step(std::integral_constant<int, 1>{})) parity ^= 1u;
+#else
+  // one loop body: the stage index is a runtime value
+  for (int s = 0; step(s); s ^= 1) parity ^= (uint32_t)s;
+#endif
   __syncwarp();
   for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
 }
@@ -622,6 +639,12 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
       alpha_d, p.rule, DT,
       tie_direction(alpha_d, overridden ? 0.0 : *p.d_amax, p.mcap, DT, overridden));
 
+  // per-tensor table of the per-scale-code reciprocals (block46)
+  __shared__ __align__(16) float4 sctab[128];
+  static_assert(kWarps * 32 >= 128, "one thread per scale code");
+  if (threadIdx.x < 128) sctab[threadIdx.x] = scale_entry(threadIdx.x, tc.alpha);
+  __syncthreads();
+  const uint32_t tab = smem_u32(sctab);
   const uint32_t wsm = smem_u32(smem) + warp * (kStages * kTileBytes);
   uint64_t* wb = bars[warp];
   uint32_t* dl = defer[warp];
@@ -645,36 +668,36 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
     if constexpr (DT == DT_BF16) {
       switch (tc.tdir) {
         case -1:
-          stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
-          stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 1:
-          stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         default:
-          stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+          stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
       }
     } else {
-      stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg);
+      stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if constexpr (DT == DT_BF16) {
     switch (tc.tdir) {
       case -1:
-        seg_stream<DT, MODE, EXTRA, -1>(p, tc, wsm, wb, dl, t_begin, t_end);
+        seg_stream<DT, MODE, EXTRA, -1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 0:
-        seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end);
+        seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 1:
-        seg_stream<DT, MODE, EXTRA, 1>(p, tc, wsm, wb, dl, t_begin, t_end);
+        seg_stream<DT, MODE, EXTRA, 1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       default:
-        seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end);
+        seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
     }
   } else {
-    seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end);
+    seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
   }
   // tcgen05 layout padding: kb in [nb, 4*kb4) of every row, rows up to a multiple of 128
   const uint32_t rows = (uint32_t)p.rows, rows_pad = (rows + 127) & ~127u;
