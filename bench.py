@@ -213,52 +213,37 @@ def moe_tensors(dev, E=None, T=None, H=None, F=None):
 
 def moe_step(t, cfg, out_dtype=None):
     """One MoE expert fwd/bwd step of the 4/6 recipe (reference qlinear.py:
-    107-159) for E experts: quantize every operand with 4/6 (X, dY 1-D along
-    the contraction dim; W1, W2 in 16x16 tiles giving W and W^T; the WGRAD
-    operands through the 16-wide RHT along tokens), then the six grouped
-    NVFP4 GEMMs.  Returns {name: C [E, M, N]} and the quantized operands."""
+    107-159) for E experts: quantize every operand with 4/6 (X, H, dY, dH 1-D
+    along the contraction dim; W1, W2 in 16x16 tiles giving W and W^T; the
+    WGRAD operands transposed through the 16-wide RHT along tokens), each
+    expert with its own tensor scale, one grouped launch per operand kind;
+    then the six grouped NVFP4 GEMMs.  Returns {name: C [E, M, N]} and the
+    plan {name: (A, B, M, N, K)} of GroupedQuantized operands."""
     import torch
 
     import paper_2512_02010_b200 as f46
 
     out_dtype = out_dtype or torch.bfloat16
-    E = t["x"].shape[0]
     spec = f46.RhtSpec(seed=cfg.seed)
-
-    def q1(a, tag=0):
-        return [f46.quantize_tensor_adaptive(a[e], cfg, sr_tag=tag, check_finite=False)
-                for e in range(E)]
-
-    def q2(w):
-        return [f46.quantize_weights_2d(w[e], cfg, check_finite=False) for e in range(E)]
-
-    def qrht(a, tag):
-        # WGRAD operand: RHT along the token axis of a^T, then 4/6 along tokens
-        return [f46.quantize_tensor_adaptive(f46.apply_rht(a[e].T.contiguous(), spec), cfg,
-                                             sr_tag=tag, check_finite=False) for e in range(E)]
-
-    def stack(qs):
-        return (torch.stack([q.packed_codes for q in qs]), torch.stack([q.scales_tc for q in qs]),
-                torch.cat([q.alpha_dev for q in qs]))
-
-    xq, hq, dyq, dhq = q1(t["x"]), q1(t["h"]), q1(t["dy"], 1), q1(t["dh"], 1)
+    q1 = lambda a: f46.quantize_grouped(a, cfg, check_finite=False)
+    q2 = lambda w: f46.quantize_weights_2d_grouped(w, cfg, check_finite=False)
+    qrht = lambda a: f46.quantize_wgrad_operand_grouped(a, cfg, spec, check_finite=False)
+    xq, hq, dyq, dhq = q1(t["x"]), q1(t["h"]), q1(t["dy"]), q1(t["dh"])
     w1, w2 = q2(t["W1"]), q2(t["W2"])
-    w1t, w2t = [q.transposed for q in w1], [q.transposed for q in w2]
-    dyT, hT, dhT, xT = qrht(t["dy"], 2), qrht(t["h"], 3), qrht(t["dh"], 2), qrht(t["x"], 3)
+    dyT, hT, dhT, xT = qrht(t["dy"]), qrht(t["h"]), qrht(t["dh"]), qrht(t["x"])
     T, H = t["x"].shape[1:]
     F = t["h"].shape[2]
     plan = {
         "fprop_x_w1": (xq, w1, T, F, H),
         "fprop_h_w2": (hq, w2, T, H, F),
-        "dgrad_dy_w2": (dyq, w2t, T, F, H),
-        "dgrad_dh_w1": (dhq, w1t, T, H, F),
+        "dgrad_dy_w2": (dyq, w2.transposed, T, F, H),
+        "dgrad_dh_w1": (dhq, w1.transposed, T, H, F),
         "wgrad_dy_h": (dyT, hT, H, F, T),
         "wgrad_dh_x": (dhT, xT, F, H, T),
     }
     outs = {}
     for name, (a, b, M, N, K) in plan.items():
-        A, B = stack(a), stack(b)
-        outs[name] = f46.gemm_nvfp4_grouped(A[0], A[1], A[2], B[0], B[1], B[2], M, N, K, out_dtype)
+        outs[name] = f46.gemm_nvfp4_grouped(*a.operands(), *b.operands(), M, N, K, out_dtype)
     return outs, plan
 
 
@@ -815,15 +800,9 @@ def bench_moe(args, dev):
     stream = torch.cuda.current_stream()
     _, plan = moe_step(t, cfg)
 
-    def stack(qs):
-        return (torch.stack([q.packed_codes for q in qs]), torch.stack([q.scales_tc for q in qs]),
-                torch.cat([q.alpha_dev for q in qs]))
-
     res, tot_flops, gemm_ms = {}, 0.0, 0.0
     for name, (a, b, M, N, K) in plan.items():
-        A, B = stack(a), stack(b)
-        run = lambda: f46.gemm_nvfp4_grouped(A[0], A[1], A[2], B[0], B[1], B[2], M, N, K,
-                                             torch.bfloat16)
+        run = lambda: f46.gemm_nvfp4_grouped(*a.operands(), *b.operands(), M, N, K, torch.bfloat16)
         ms = timed_back_to_back(run, stream, 5, warm=3)
         fl = 2.0 * E * M * N * K
         res[name] = {"M": M, "N": N, "K": K, "experts": E, "ms": ms, "TFLOP/s": fl / (ms * 1e-3) / 1e12}

@@ -17,6 +17,8 @@
  *   f46_quantize_2d     transforms.py:134-179  quantize_weights_2d (16x16 tiles)
  *   f46_dequantize      blockquant.py:363-376  dequantize_tensor
  *   f46_gemm_nvfp4      qlinear.py:74-93       emulated_fp4_matmul(aq, bq, transpose_b=True)
+ *   f46_*_grouped       the above per MoE expert (one tensor scale per expert), one launch
+ *   f46_quantize_rht_t_grouped  qlinear.py:150-157  apply_rht(a.T) + _quantize_1d (WGRAD operand)
  *
  * Data layout written by f46_quantize for a tensor viewed as [rows, cols]
  * (cols = last dimension, 16-element blocks along it, nb = ceil(cols/16)):
@@ -215,6 +217,47 @@ int f46_quantize_sr(const void* x, int dtype, int64_t rows, int64_t cols, int mo
  */
 int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double* out,
               f46_stream_t stream);
+
+/*
+ * Grouped (expert-parallel MoE) variants.  A grouped
+ * tensor is `groups` equal tensors stored back to back; each group is its own
+ * reference tensor with its own tensor scale (d_amax[g], d_alpha_out[g]), i.e.
+ * exactly what a per-group call of the single-tensor function would produce
+ * (blockquant.py:215-222 per expert), in one launch.  Output buffers are the
+ * per-group buffers back to back (group stride f46_codes_bytes(rows, cols) /
+ * f46_scales_tc_bytes(rows, cols)) -- the operand packing of
+ * f46_gemm_nvfp4_grouped.  The caller zeroes d_amax[groups] before the amax
+ * call.
+ */
+int f46_amax_grouped(const void* x, int dtype, int groups, int64_t n, double* d_amax,
+                     f46_stream_t stream);
+/* f46_quantize per group (no alpha override, no parity views). */
+int f46_quantize_grouped(const void* x, int dtype, int groups, int64_t rows, int64_t cols, int mode,
+                         int rule, double mcap, const double* d_amax, uint8_t* codes,
+                         uint8_t* scales_tc, double* d_alpha_out, uint32_t* d_flags,
+                         f46_stream_t stream);
+/* f46_quantize_2d per group (W and, if non-null, W^T); scale buffers zeroed by the caller. */
+int f46_quantize_2d_grouped(const void* w, int dtype, int groups, int64_t R, int64_t C, int mode,
+                            int rule, double mcap, const double* d_amax, uint8_t* codes,
+                            uint8_t* scales_tc, uint8_t* codes_t, uint8_t* scales_tc_t,
+                            double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream);
+
+/*
+ * WGRAD operand in one fused pass (qlinear.py:138-159): for each group's
+ * row-major a[T][H] (T % 16 == 0), the operand A = RHT16 along T of a^T,
+ * i.e. apply_rht(a.T, spec) (transforms.py:92-97, float64, numpy's butterfly
+ * order), quantized 1-D along T with the given mode -- an [H][T] container
+ * (codes [H][T/16*8], tcgen05 scales of [H, T], zeroed by the caller).
+ * sign_mask bit i = 1 where spec.signs[i] == -1.  f46_rht_t_amax_grouped
+ * folds max|A| per group into d_amax[g] (zeroed by the caller); the quantize
+ * call reads it.  BF16 or FP32 input.
+ */
+int f46_rht_t_amax_grouped(const void* a, int dtype, int groups, int64_t T, int64_t H,
+                           uint32_t sign_mask, double* d_amax, f46_stream_t stream);
+int f46_quantize_rht_t_grouped(const void* a, int dtype, int groups, int64_t T, int64_t H,
+                               uint32_t sign_mask, int mode, int rule, double mcap,
+                               double* d_amax, uint8_t* codes, uint8_t* scales_tc,
+                               double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream);
 
 /* Human-readable build info ("sm_100a ..."). */
 const char* f46_build_info(void);

@@ -196,3 +196,24 @@ def bf16_bits(x_f32: np.ndarray) -> np.ndarray:
 
 def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
     return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def apply_rht(x: np.ndarray, signs: np.ndarray) -> np.ndarray:
+    """transforms.py:76-97 apply_rht restated: per contiguous group of 16
+    along the last axis, y = fwht(g * signs) / sqrt(16) in float64, with the
+    reference's butterfly order (h = 1, 2, 4, 8; top = a[j] + a[j+h],
+    bot = a[j] - a[j+h] within each 2h-block).  Every output is the same single
+    IEEE operation on the same operands as the reference's, so it is bit-exact."""
+    a = np.asarray(x, dtype=np.float64)
+    n = a.shape[-1]
+    if n % 16:
+        raise ValueError("oracle: last dimension must be a multiple of 16")
+    g = a.reshape(-1, 16) * np.asarray(signs, dtype=np.float64)
+    h = 1
+    while h < 16:
+        g = g.reshape(-1, 16 // (2 * h), 2, h)
+        top = g[:, :, 0, :] + g[:, :, 1, :]
+        bot = g[:, :, 0, :] - g[:, :, 1, :]
+        g = np.stack([top, bot], axis=2).reshape(-1, 16)
+        h *= 2
+    return (g / np.sqrt(16.0)).reshape(a.shape)

@@ -44,6 +44,11 @@ EXPORTS = (
     "f46_selection_stats",
     "f46_quantize_sr",
     "f46_rht16",
+    "f46_amax_grouped",
+    "f46_quantize_grouped",
+    "f46_quantize_2d_grouped",
+    "f46_rht_t_amax_grouped",
+    "f46_quantize_rht_t_grouped",
     "f46_build_info",
 )
 
@@ -81,6 +86,17 @@ def _declare(L):
     L.f46_quantize_sr.restype = i
     L.f46_rht16.argtypes = [p, i, i64, p, p, p]
     L.f46_rht16.restype = i
+    L.f46_amax_grouped.argtypes = [p, i, i, i64, p, p]
+    L.f46_amax_grouped.restype = i
+    L.f46_quantize_grouped.argtypes = [p, i, i, i64, i64, i, i, d, p, p, p, p, p, p]
+    L.f46_quantize_grouped.restype = i
+    L.f46_quantize_2d_grouped.argtypes = [p, i, i, i64, i64, i, i, d, p, p, p, p, p, p, p, p]
+    L.f46_quantize_2d_grouped.restype = i
+    u32 = ctypes.c_uint32
+    L.f46_rht_t_amax_grouped.argtypes = [p, i, i, i64, i64, u32, p, p]
+    L.f46_rht_t_amax_grouped.restype = i
+    L.f46_quantize_rht_t_grouped.argtypes = [p, i, i, i64, i64, u32, i, i, d, p, p, p, p, p, p]
+    L.f46_quantize_rht_t_grouped.restype = i
     L.f46_build_info.argtypes = []
     L.f46_build_info.restype = ctypes.c_char_p
 

@@ -263,14 +263,14 @@ __device__ __forceinline__ void exact_block_inl(const double* xin, double alpha,
   }
 }
 
-__device__ __noinline__ void exact_block(const double* xin, double alpha, int mode, int rule,
+static __device__ __noinline__ void exact_block(const double* xin, double alpha, int mode, int rule,
                                          BlockOut* out) {
   exact_block_inl(xin, alpha, mode, rule, out);
 }
 
 // Exact float64 squared-error sum of one candidate whose codes are known
 // (blockquant.py:279, :289-290), used when the f32 comparison is ambiguous.
-__device__ __noinline__ double exact_sq_sum(const double* x, uint64_t codes, double alpha,
+static __device__ __noinline__ double exact_sq_sum(const double* x, uint64_t codes, double alpha,
                                             double delta) {
   const double denom = __dmul_rn(alpha, delta);
   double e[16];

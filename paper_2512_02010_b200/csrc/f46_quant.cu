@@ -100,7 +100,22 @@ struct QParams {
   uint8_t* pick4;
   double* d_alpha_out;
   uint32_t* d_flags;
+  // grouped launches (gridDim.y groups): per-group strides of x (bytes), codes
+  // and scales_tc (bytes); d_amax / d_alpha_out are indexed by the group
+  int64_t g_x, g_codes, g_scales;
 };
+
+// Point the parameters at group blockIdx.y of a grouped launch.
+__device__ __forceinline__ void select_group(QParams& p) {
+  if (gridDim.y > 1) {
+    const int64_t g = blockIdx.y;
+    p.x = reinterpret_cast<const uint8_t*>(p.x) + g * p.g_x;
+    p.codes += g * p.g_codes;
+    p.scales_tc += g * p.g_scales;
+    if (p.d_amax) p.d_amax += g;
+    if (p.d_alpha_out) p.d_alpha_out += g;
+  }
+}
 
 // blockquant.py:215-222 / :316-326: alpha = RN32(f32(amax) / f32(mcap)), 1.0
 // for an all-zero tensor, or the override.
@@ -622,6 +637,7 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   __shared__ __align__(8) uint64_t bars[kWarps][kStages];
   __shared__ uint32_t defer[kWarps][kDefer];
 
+  select_group(p);
   // warp index through a shuffle: the compiler then knows it is warp-uniform
   const int warp = __shfl_sync(0xFFFFFFFFu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t cols = (uint32_t)p.cols;
@@ -735,6 +751,7 @@ struct GlobalLoad {
 
 template <int DT, int MODE>
 __global__ void __launch_bounds__(256) quant_generic_kernel(QParams p) {
+  select_group(p);
   const int64_t nb = (p.cols + 15) >> 4;
   const int64_t kb4 = (nb + 3) >> 2;
   const int64_t rows_pad = (p.rows + 127) & ~(int64_t)127;
@@ -824,7 +841,21 @@ struct Q2Params {
   uint8_t* scales_tc_t;  // tcgen05 layout of [C, R] (nullable)
   double* d_alpha_out;
   uint32_t* d_flags;
+  int64_t g_w, g_codes, g_scales, g_codes_t, g_scales_t;  // grouped launches (bytes)
 };
+
+__device__ __forceinline__ void select_group2(Q2Params& p) {
+  if (gridDim.y > 1) {
+    const int64_t g = blockIdx.y;
+    p.w = reinterpret_cast<const uint8_t*>(p.w) + g * p.g_w;
+    p.codes += g * p.g_codes;
+    p.scales_tc += g * p.g_scales;
+    if (p.codes_t) p.codes_t += g * p.g_codes_t;
+    if (p.scales_tc_t) p.scales_tc_t += g * p.g_scales_t;
+    if (p.d_amax) p.d_amax += g;
+    if (p.d_alpha_out) p.d_alpha_out += g;
+  }
+}
 
 __device__ __forceinline__ double q2_load(const Q2Params& p, int64_t r, int64_t c) {
   if (r >= p.R || c >= p.C) return 0.0;
@@ -909,6 +940,7 @@ __device__ __forceinline__ uint32_t tile_codes8(const float (&xf)[8], float alph
 #define F46_Q2_MINB 4
 #endif
 __global__ void __launch_bounds__(256, F46_Q2_MINB) quant2d_kernel(Q2Params p) {
+  select_group2(p);
   __shared__ double esq[8][256];   // the rule's per-element errors of one candidate
   __shared__ double dtab[8][16];    // dequantized value of each code under the candidate
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1158,6 +1190,7 @@ __device__ __noinline__ void quant2d_tile_exact(const Q2Params p, double alpha, 
 #define F46_Q2V2_MINB 4
 #endif
 __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params p) {
+  select_group2(p);
   const int lane = threadIdx.x & 31, hw = lane >> 4, l = lane & 15, h = l >> 3, j = l & 7;
   const int hbase = lane & 16;
   const unsigned FULL = 0xFFFFFFFFu;
@@ -1919,6 +1952,11 @@ __global__ void __launch_bounds__(256) rht16_kernel(const void* __restrict__ x, 
 template <int DT>
 __global__ void __launch_bounds__(256) amax_kernel(const void* __restrict__ x, int64_t n,
                                                    double* d_amax) {
+  if (gridDim.y > 1) {  // grouped: group blockIdx.y of n elements each
+    constexpr int64_t kEsz = DT == DT_BF16 ? 2 : (DT == DT_F32 ? 4 : 8);
+    x = reinterpret_cast<const uint8_t*>(x) + (int64_t)blockIdx.y * n * kEsz;
+    d_amax += blockIdx.y;
+  }
   uint64_t m64 = 0;  // float64 |x| bit pattern (non-negative: bit order == value order)
   uint32_t m32 = 0;  // float32 |x| bit pattern
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -2570,7 +2608,7 @@ int launch_status() {
 }
 
 template <int DT, int MODE, bool EXTRA>
-int launch_quant_seg(const QParams& p, cudaStream_t s) {
+int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
   constexpr int kTileBytes = kSegElems * ((DT == DT_BF16) ? 2 : 4);
   const int smem = kWarps * kStages * kTileBytes;
   static bool configured = false;
@@ -2594,6 +2632,15 @@ int launch_quant_seg(const QParams& p, cudaStream_t s) {
   }
   int64_t rows_max = (chunk_bytes / (p.cols * kEsz)) & ~(int64_t)127;
   if (rows_max < 128) return F46_ERR_UNSUPPORTED;
+  if (groups > 1) {  // one launch, group = blockIdx.y; each group within one slab
+    if (p.rows > rows_max) return F46_ERR_UNSUPPORTED;
+    const int64_t tiles = p.rows * ((p.cols + kSegElems - 1) / kSegElems);
+    int64_t grid = ((int64_t)num_sms() * ctas_per_sm + groups - 1) / groups;
+    grid = std::min(grid, (tiles + kWarps - 1) / kWarps);
+    if (grid < 1) grid = 1;
+    quant_seg_kernel<DT, MODE, EXTRA><<<dim3((unsigned)grid, (unsigned)groups), kWarps * 32, smem, s>>>(p);
+    return launch_status();
+  }
   for (int64_t r0 = 0; r0 < p.rows; r0 += rows_max) {
     QParams q = p;
     q.rows = std::min(rows_max, p.rows - r0);
@@ -2612,33 +2659,33 @@ int launch_quant_seg(const QParams& p, cudaStream_t s) {
 }
 
 template <int DT, int MODE>
-int launch_quant_generic(const QParams& p, cudaStream_t s) {
+int launch_quant_generic(const QParams& p, cudaStream_t s, int groups = 1) {
   const int64_t nb = (p.cols + 15) >> 4;
   const int64_t total = ((p.rows + 127) & ~(int64_t)127) * (((nb + 3) >> 2) * 4);
   int64_t grid = (total + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const int64_t cap = std::max<int64_t>(1, (int64_t)num_sms() * 8 / groups);
   if (grid > cap) grid = cap;
-  quant_generic_kernel<DT, MODE><<<(unsigned)grid, 256, 0, s>>>(p);
+  quant_generic_kernel<DT, MODE><<<dim3((unsigned)grid, (unsigned)groups), 256, 0, s>>>(p);
   return launch_status();
 }
 
 template <int DT, int MODE>
-int launch_quant(const QParams& p, cudaStream_t s, bool tma) {
-  if (!tma) return launch_quant_generic<DT, MODE>(p, s);
+int launch_quant(const QParams& p, cudaStream_t s, bool tma, int groups = 1) {
+  if (!tma) return launch_quant_generic<DT, MODE>(p, s, groups);
   // parity views (row-major scales, 4/6 choice) get their own instantiation
-  return (p.scales_rm || p.pick4) ? launch_quant_seg<DT, MODE, true>(p, s)
-                                  : launch_quant_seg<DT, MODE, false>(p, s);
+  return (p.scales_rm || p.pick4) ? launch_quant_seg<DT, MODE, true>(p, s, groups)
+                                  : launch_quant_seg<DT, MODE, false>(p, s, groups);
 }
 
 template <int DT>
-int dispatch_mode(const QParams& p, cudaStream_t s, bool tma) {
+int dispatch_mode(const QParams& p, cudaStream_t s, bool tma, int groups = 1) {
   switch (p.mode) {
     case F46_FIXED6:
-      return launch_quant<DT, FIXED6>(p, s, tma);
+      return launch_quant<DT, FIXED6>(p, s, tma, groups);
     case F46_FIXED4:
-      return launch_quant<DT, FIXED4>(p, s, tma);
+      return launch_quant<DT, FIXED4>(p, s, tma, groups);
     default:
-      return launch_quant<DT, ADAPTIVE>(p, s, tma);
+      return launch_quant<DT, ADAPTIVE>(p, s, tma, groups);
   }
 }
 
@@ -2786,6 +2833,89 @@ int f46_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int mode,
     default:
       return F46_ERR_INVALID_ARG;
   }
+}
+
+int f46_amax_grouped(const void* x, int dtype, int groups, int64_t n, double* d_amax,
+                     f46_stream_t stream) {
+  if (!x || !d_amax || n < 0 || groups < 1 || groups > 65535) return F46_ERR_INVALID_ARG;
+  if (n == 0) return F46_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t per = dtype == F46_DT_BF16 ? 256 * 8 * 16 : 256 * 4 * 16;
+  int64_t gx = (n + per - 1) / per;
+  gx = std::min<int64_t>(gx, std::max<int64_t>(1, (int64_t)num_sms() * 8 / groups));
+  const dim3 grid((unsigned)std::max<int64_t>(gx, 1), (unsigned)groups);
+  switch (dtype) {
+    case F46_DT_BF16:
+      amax_kernel<DT_BF16><<<grid, 256, 0, s>>>(x, n, d_amax);
+      break;
+    case F46_DT_F32:
+      amax_kernel<DT_F32><<<grid, 256, 0, s>>>(x, n, d_amax);
+      break;
+    case F46_DT_F64:
+      amax_kernel<DT_F64><<<grid, 256, 0, s>>>(x, n, d_amax);
+      break;
+    default:
+      return F46_ERR_INVALID_ARG;
+  }
+  return launch_status();
+}
+
+int f46_quantize_grouped(const void* x, int dtype, int groups, int64_t rows, int64_t cols, int mode,
+                         int rule, double mcap, const double* d_amax, uint8_t* codes,
+                         uint8_t* scales_tc, double* d_alpha_out, uint32_t* d_flags,
+                         f46_stream_t stream) {
+  if (!x || !codes || !scales_tc || !d_amax || rows <= 0 || cols <= 0 || groups < 1 ||
+      groups > 65535 || !(mcap > 0.0))
+    return F46_ERR_INVALID_ARG;
+  if (mode < F46_FIXED6 || mode > F46_ADAPTIVE || rule < F46_RULE_MSE || rule > F46_RULE_ABSMAX)
+    return F46_ERR_CONFIG;
+  if (dtype != F46_DT_BF16 && dtype != F46_DT_F32 && dtype != F46_DT_F64) return F46_ERR_INVALID_ARG;
+  const int64_t esz = dtype == F46_DT_BF16 ? 2 : (dtype == F46_DT_F32 ? 4 : 8);
+  QParams p{x, rows, cols, mode, rule, dtype, mcap, d_amax, 0.0, codes, scales_tc, nullptr,
+            nullptr, d_alpha_out, d_flags, rows * cols * esz, (int64_t)f46_codes_bytes(rows, cols),
+            (int64_t)f46_scales_tc_bytes(rows, cols)};
+  cudaStream_t s = (cudaStream_t)stream;
+  // every group's base must satisfy the segment kernel's alignment as well
+  const bool tma = (dtype != F46_DT_F64) && (cols % 16 == 0) && (((uintptr_t)x & 15) == 0) &&
+                   ((p.g_x & 15) == 0) && (((uintptr_t)codes & 7) == 0) &&
+                   rows < (1ll << 31) && cols < (1ll << 31) && rows * ((cols + 15) / 16) < (1ll << 32);
+  int rc;
+  switch (dtype) {
+    case F46_DT_BF16:
+      rc = dispatch_mode<DT_BF16>(p, s, tma, groups);
+      if (rc == F46_ERR_UNSUPPORTED && tma) rc = dispatch_mode<DT_BF16>(p, s, false, groups);
+      return rc;
+    case F46_DT_F32:
+      rc = dispatch_mode<DT_F32>(p, s, tma, groups);
+      if (rc == F46_ERR_UNSUPPORTED && tma) rc = dispatch_mode<DT_F32>(p, s, false, groups);
+      return rc;
+    default:
+      return dispatch_mode<DT_F64>(p, s, false, groups);
+  }
+}
+
+int f46_quantize_2d_grouped(const void* w, int dtype, int groups, int64_t R, int64_t C, int mode,
+                            int rule, double mcap, const double* d_amax, uint8_t* codes,
+                            uint8_t* scales_tc, uint8_t* codes_t, uint8_t* scales_tc_t,
+                            double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream) {
+  if (!w || !codes || !scales_tc || !d_amax || R <= 0 || C <= 0 || groups < 1 || groups > 65535 ||
+      !(mcap > 0.0))
+    return F46_ERR_INVALID_ARG;
+  if (mode < F46_FIXED6 || mode > F46_ADAPTIVE || rule < F46_RULE_MSE || rule > F46_RULE_ABSMAX)
+    return F46_ERR_CONFIG;
+  if (dtype != F46_DT_F32 && dtype != F46_DT_BF16) return F46_ERR_INVALID_ARG;
+  if ((codes_t == nullptr) != (scales_tc_t == nullptr)) return F46_ERR_INVALID_ARG;
+  const int64_t esz = dtype == F46_DT_BF16 ? 2 : 4;
+  Q2Params p{w, R, C, mode, rule, dtype, mcap, d_amax, 0.0, codes, scales_tc, nullptr, nullptr,
+             codes_t, scales_tc_t, d_alpha_out, d_flags, R * C * esz,
+             (int64_t)f46_codes_bytes(R, C), (int64_t)f46_scales_tc_bytes(R, C),
+             (int64_t)f46_codes_bytes(C, R), (int64_t)f46_scales_tc_bytes(C, R)};
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t tiles = ((R + 15) / 16) * ((C + 15) / 16);
+  int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
+  g2 = std::min<int64_t>(g2, std::max<int64_t>(1, (int64_t)num_sms() * 8 / groups));
+  quant2d_v2_kernel<<<dim3((unsigned)std::max<int64_t>(g2, 1), (unsigned)groups), 256, 0, s>>>(p);
+  return launch_status();
 }
 
 int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout,

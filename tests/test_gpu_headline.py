@@ -136,7 +136,8 @@ def test_c5_moe_step_all_shapes():
         C = outs[name]
         assert C.shape == (E, M, N), name
         for e in range(E):
-            ref = f46.dequantize_tensor(a[e], torch.float64) @ f46.dequantize_tensor(b[e], torch.float64).T
+            ref = (f46.dequantize_tensor(a.group(e), torch.float64)
+                   @ f46.dequantize_tensor(b.group(e), torch.float64).T)
             assert rel_fro(C[e], ref) <= REL_TOL, (name, e)
 
 
@@ -148,13 +149,22 @@ def test_c5_operands_match_oracle_one_expert():
     t = bench.moe_tensors(dev, E=1)
     _, plan = bench.moe_step(t, cfg)
     x = t["x"][0]
-    xq = plan["fprop_x_w1"][0][0]
+    xq = plan["fprop_x_w1"][0].group(0)
     ref = O.quantize(bits_of(x), "adaptive")
     assert np.array_equal(xq.packed_codes.cpu().numpy(), ref["codes"])
     assert np.array_equal(xq.scale_codes, ref["scales"])
     w = t["W1"][0]
-    wq = plan["fprop_x_w1"][1][0]
+    wq = plan["fprop_x_w1"][1].group(0)
     r2 = O.quantize_2d(bits_of(w), "adaptive")
     assert wq.alpha == r2["alpha"]
     assert np.array_equal(wq.packed_codes.cpu().numpy(), r2["codes"])
     assert np.array_equal(wq.scale_codes, r2["scales"])
+    # WGRAD operand: apply_rht(dy.T) along tokens, then 4/6 (qlinear.py:150-157)
+    dy = t["dy"][0].cpu()
+    spec = f46.RhtSpec(seed=cfg.seed)
+    y = O.apply_rht(np.ascontiguousarray(dy.float().double().numpy().T), spec.signs)
+    r3 = O.quantize(y, "adaptive")
+    aq = plan["wgrad_dy_h"][0].group(0)
+    assert aq.alpha == r3["alpha"]
+    assert np.array_equal(aq.packed_codes.cpu().numpy(), r3["codes"])
+    assert np.array_equal(aq.scale_codes, r3["scales"])
