@@ -1189,8 +1189,13 @@ __device__ __noinline__ void quant2d_tile_exact(const Q2Params p, double alpha, 
 #ifndef F46_Q2V2_MINB
 #define F46_Q2V2_MINB 4
 #endif
+constexpr int kQ2Row = 24;  // staged tile row stride (bf16): 48 bytes, 16-byte aligned
+
+// MSE: the rule is the squared error (the default) -- no |diff| maximum.
+template <bool MSE>
 __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params p) {
   select_group2(p);
+  __shared__ __align__(16) uint16_t stage[8][2][16 * kQ2Row];
   const int lane = threadIdx.x & 31, hw = lane >> 4, l = lane & 15, h = l >> 3, j = l & 7;
   const int hbase = lane & 16;
   const unsigned FULL = 0xFFFFFFFFu;
@@ -1222,10 +1227,28 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
     const int64_t r0 = tr * 16 + 8 * h, c0 = tc * 16;
     // the lane's 16 values in accumulation order: (row r0 + i/2, col (i%2)*8 + j)
     float x[16];
+    // interior BF16 tiles: the half-warp stages its 16x16 tile through shared
+    // memory with two 16-byte loads per lane (lane l: row l of the tile)
+    const bool staged = live && p.dtype == DT_BF16 && (p.C & 7) == 0 && tr * 16 + 16 <= p.R &&
+                        c0 + 16 <= p.C && ((reinterpret_cast<uintptr_t>(p.w) & 15) == 0);
+    if (__all_sync(FULL, staged)) {
+      uint16_t* st = stage[threadIdx.x >> 5][hw];
+      const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.w) +
+                                                        (tr * 16 + l) * p.C + c0);
+      const uint4 v0 = __ldcs(src), v1 = __ldcs(src + 1);
+      reinterpret_cast<uint4*>(st + l * kQ2Row)[0] = v0;
+      reinterpret_cast<uint4*>(st + l * kQ2Row)[1] = v1;
+      __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int64_t r = r0 + (i >> 1), c = c0 + ((i & 1) << 3) + j;
-      x[i] = live ? (float)q2_load(p, r, c) : 0.f;
+      for (int i = 0; i < 16; ++i)
+        x[i] = __uint_as_float((uint32_t)st[(8 * h + (i >> 1)) * kQ2Row + ((i & 1) << 3) + j] << 16);
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + (i >> 1), c = c0 + ((i & 1) << 3) + j;
+        x[i] = live ? (float)q2_load(p, r, c) : 0.f;
+      }
     }
     uint32_t mb = 0;
 #pragma unroll
@@ -1270,12 +1293,12 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
       for (int i = 0; i < 16; ++i) {
         const double diff = __dsub_rn(__dmul_rn(dec_fp4_d((uint32_t)(codes >> (4 * i)) & 15u), denom),
                                       (double)x[i]);
-        const double e = p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff);
+        const double e = MSE ? __dmul_rn(diff, diff) : (p.rule == RULE_MSE ? __dmul_rn(diff, diff) : fabs(diff));
         r = i == 0 ? e : __dadd_rn(r, e);
-        mx = fmax(mx, fabs(diff));
+        if (!MSE) mx = fmax(mx, fabs(diff));
       }
       double tot;
-      if (p.rule == RULE_ABSMAX) {
+      if (!MSE && p.rule == RULE_ABSMAX) {
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
         tot = mx;
@@ -2914,7 +2937,10 @@ int f46_quantize_2d_grouped(const void* w, int dtype, int groups, int64_t R, int
   const int64_t tiles = ((R + 15) / 16) * ((C + 15) / 16);
   int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
   g2 = std::min<int64_t>(g2, std::max<int64_t>(1, (int64_t)num_sms() * 8 / groups));
-  quant2d_v2_kernel<<<dim3((unsigned)std::max<int64_t>(g2, 1), (unsigned)groups), 256, 0, s>>>(p);
+  if (rule == F46_RULE_MSE)
+    quant2d_v2_kernel<true><<<dim3((unsigned)std::max<int64_t>(g2, 1), (unsigned)groups), 256, 0, s>>>(p);
+  else
+    quant2d_v2_kernel<false><<<dim3((unsigned)std::max<int64_t>(g2, 1), (unsigned)groups), 256, 0, s>>>(p);
   return launch_status();
 }
 
@@ -2995,7 +3021,10 @@ int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, in
     const int64_t cap2 = (int64_t)num_sms() * 8;
     if (g2 > cap2) g2 = cap2;
     if (g2 < 1) g2 = 1;
-    quant2d_v2_kernel<<<(unsigned)g2, 256, 0, s>>>(p);
+    if (rule == F46_RULE_MSE)
+      quant2d_v2_kernel<true><<<(unsigned)g2, 256, 0, s>>>(p);
+    else
+      quant2d_v2_kernel<false><<<(unsigned)g2, 256, 0, s>>>(p);
   } else {
     quant2d_kernel<<<(unsigned)grid, 256, 0, s>>>(p);
   }

@@ -46,6 +46,7 @@ struct RtParams {
   double* d_alpha_out;  // [groups] (nullable)
   uint32_t* d_flags;    // nullable
   int64_t g_a, g_codes, g_scales;  // per-group strides (bytes)
+  float sq[16];  // signs[i] / 4 (exact): the f32 route's per-token factor
 };
 
 __device__ __forceinline__ void select_group(RtParams& p) {
@@ -129,6 +130,51 @@ __device__ __forceinline__ void rht16(double (&a)[16], uint32_t negmask) {
   for (int i = 0; i < 16; ++i) a[i] = __dmul_rn(a[i], 0.25);
 }
 
+// BF16 input, both features of the lane at once in f32x2 (a[i] = (feature
+// h0, feature h0+1) of token i).  Every operation is exact -- so the result
+// equals the float64 route bit for bit -- when, per feature, the nonzero
+// inputs span at most 12 binades (any partial sum of <= 16 terms then needs
+// <= 8 + 12 + 4 = 24 significant bits) and none is below 2^-99 (x/4 and all
+// sums stay normal).  ok0 / ok1 report the condition per feature; callers take
+// the float64 route otherwise.  The signs and the /4 fold into one exact
+// product per token.
+__device__ __forceinline__ void rht16_pair_f32(const uint32_t (&w)[16], const float (&sq)[16],
+                                               float2 (&a)[16], bool& ok0, bool& ok1) {
+  uint32_t mx = 0, mn = 0xFFFFFFFFu;  // per half: max |bits|, min(|bits| - 1) (zeros wrap high)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t m = w[i] & 0x7FFF7FFFu;
+    mx = __vmaxu2(mx, m);
+    mn = __vminu2(mn, __vsub2(m, 0x00010001u));
+  }
+  const int e0max = (mx & 0xFFFFu) >> 7, e1max = mx >> 23;
+  const int e0min = ((mn & 0xFFFFu) + 1) >> 7, e1min = ((mn >> 16) + 1) >> 7;
+  // all-zero feature: emin = 512 > emax (exact); else span and range checks
+  ok0 = (e0max - e0min <= 12) && (e0min >= 28);
+  ok1 = (e1max - e1min <= 12) && (e1min >= 28);
+  ok0 |= e0min == 512;
+  ok1 |= e1min == 512;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float2 x = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+    a[i] = __fmul2_rn(x, make_float2(sq[i], sq[i]));
+  }
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1) {
+    float2 b[16];
+#pragma unroll
+    for (int blk = 0; blk < 16; blk += 2 * h)
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const float2 u = a[blk + j], v = a[blk + h + j];
+        b[blk + j] = __fadd2_rn(u, v);
+        b[blk + h + j] = __fadd2_rn(u, make_float2(-v.x, -v.y));
+      }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = b[i];
+  }
+}
+
 __device__ __forceinline__ uint64_t absbits(double v) {
   return (uint64_t)__double_as_longlong(v) & 0x7FFFFFFFFFFFFFFFull;
 }
@@ -149,8 +195,23 @@ __global__ void __launch_bounds__(256, 2) rht_t_amax_kernel(RtParams p) {
       if (k >= nbT) break;
       Col2<DT> c;
       load_pair<DT>(p, k, h0, c);
+      bool ok[2] = {false, false};
+      if constexpr (DT == DT_BF16) {
+        float2 a[16];
+        rht16_pair_f32(c.w, p.sq, a, ok[0], ok[1]);
+        uint32_t m0 = 0, m1 = 0;  // |y| f32 bit patterns
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          m0 = max(m0, __float_as_uint(a[i].x) & 0x7FFFFFFFu);
+          m1 = max(m1, __float_as_uint(a[i].y) & 0x7FFFFFFFu);
+        }
+        const uint64_t b0 = absbits((double)__uint_as_float(m0)), b1 = absbits((double)__uint_as_float(m1));
+        if (ok[0]) m = b0 > m ? b0 : m;
+        if (ok[1]) m = b1 > m ? b1 : m;
+      }
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
+        if (ok[f]) continue;
         double v[16];
         column<DT>(c, f, v);
         rht16(v, p.negmask);
@@ -190,31 +251,54 @@ struct RegLoad {
   }
 };
 
+// Fast path of one block: y as float32 (all 16 values must be exact) through
+// block_sl.  False: the block is deferred to the float64 restatement.
 template <int MODE>
-__device__ __forceinline__ BlockOut quant_block_f64(const double (&y)[16], const TensorConsts& tc,
-                                                    double alpha_d, int mode, int rule) {
+__device__ __forceinline__ bool quant_block_fast(const double (&y)[16], const TensorConsts& tc,
+                                                 BlockOut& o) {
   float2 xf[8];
-  bool f32ok = true;
+  bool f32ok = !tc.force_exact;
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     xf[p] = make_float2(__double2float_rn(y[2 * p]), __double2float_rn(y[2 * p + 1]));
     f32ok &= ((double)xf[p].x == y[2 * p]) & ((double)xf[p].y == y[2 * p + 1]);
   }
-  BlockOut o;
-  bool ok = false;
-  if (f32ok && !tc.force_exact) {
-    float m0 = 0.f;
+  float m0 = 0.f;
 #pragma unroll
-    for (int p = 0; p < 8; ++p) m0 = fmaxf(m0, fmaxf(fabsf(xf[p].x), fabsf(xf[p].y)));
-    ok = block_sl<MODE, 2>(xf, m0, tc, RegLoad{xf}, o);
+  for (int p = 0; p < 8; ++p) m0 = fmaxf(m0, fmaxf(fabsf(xf[p].x), fabsf(xf[p].y)));
+  return block_sl<MODE, 2>(xf, m0, tc, RegLoad{xf}, o) && f32ok;
+}
+
+constexpr int kRtDeferCta = 4096;  // deferred (h, k) per CTA
+
+template <int DT>
+__device__ __noinline__ void rt_resolve(const RtParams p, double alpha_d, uint32_t hk, int64_t kb4) {
+  const int64_t h = hk >> 16, k = hk & 0xFFFFu;
+  const int64_t t0 = k * 16;
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if constexpr (DT == DT_BF16)
+      v[i] = (double)__uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(p.a)[(t0 + i) * p.H + h] << 16);
+    else
+      v[i] = (double)reinterpret_cast<const float*>(p.a)[(t0 + i) * p.H + h];
   }
-  if (!ok) exact_block(y, alpha_d, mode, rule, &o);
-  return o;
+  rht16(v, p.negmask);
+  BlockOut o;
+  exact_block(v, alpha_d, p.mode, p.rule, &o);
+  *reinterpret_cast<uint64_t*>(p.codes + h * (p.T >> 4) * 8 + k * 8) = o.codes;
+  p.scales_tc[sf_tc_offset(h, k, kb4)] = (uint8_t)o.sc;
 }
 
 template <int DT, int MODE>
 __global__ void __launch_bounds__(256, F46_RT_MINB) quant_rht_t_kernel(RtParams p) {
   select_group(p);
+  // blocks for the float64 route, CTA-wide: resolved by all 256 threads at the
+  // end (a few per warp would otherwise run with most lanes idle)
+  __shared__ uint32_t dlist[kRtDeferCta];
+  __shared__ uint32_t ndef;
+  if (threadIdx.x == 0) ndef = 0;
+  __syncthreads();
   const double amax = *p.d_amax;
   const double alpha_d = amax == 0.0 ? 1.0 : (double)((float)amax / (float)p.mcap);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -227,30 +311,66 @@ __global__ void __launch_bounds__(256, F46_RT_MINB) quant_rht_t_kernel(RtParams 
   const int64_t nH = (p.H + kUnitH - 1) / kUnitH, nK = (nbT + kUnitK - 1) / kUnitK;
   const int64_t units = nH * nK;
   const int lane = threadIdx.x & 31;
+  const int64_t row_bytes = nbT * 8;
   for (int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * 8) {
     const int64_t hu = u % nH, ku = u / nH;
     const int64_t h0 = hu * kUnitH + 2 * lane;
-    const int64_t row_bytes = nbT * 8;
 #pragma unroll 1
     for (int kk = 0; kk < kUnitK; ++kk) {
       const int64_t k = ku * kUnitK + kk;
       if (k >= nbT) break;
       Col2<DT> c;
       load_pair<DT>(p, k, h0, c);
+      float2 a[16];
+      bool okf[2] = {false, false};
+      if constexpr (DT == DT_BF16) rht16_pair_f32(c.w, p.sq, a, okf[0], okf[1]);
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
         const int64_t h = h0 + f;
-        double v[16];
-        column<DT>(c, f, v);
-        rht16(v, p.negmask);
-        const BlockOut o = quant_block_f64<MODE>(v, tc, alpha_d, p.mode, p.rule);
-        if (h < p.H) {
+        BlockOut o;
+        bool ok;
+        if constexpr (DT == DT_BF16) {
+          // the f32 route's values are the reference's float64 values exactly
+          float2 xf[8];
+          float bm = 0.f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            xf[q] = f ? make_float2(a[2 * q].y, a[2 * q + 1].y) : make_float2(a[2 * q].x, a[2 * q + 1].x);
+            bm = fmaxf(bm, fmaxf(fabsf(xf[q].x), fabsf(xf[q].y)));
+          }
+          ok = block_sl<MODE, 2>(xf, bm, tc, RegLoad{xf}, o) && okf[f] && !tc.force_exact;
+        } else {
+          double v[16];
+          column<DT>(c, f, v);
+          rht16(v, p.negmask);
+          ok = quant_block_fast<MODE>(v, tc, o);
+        }
+        const bool live = h < p.H;
+        if (live && ok) {
           *reinterpret_cast<uint64_t*>(p.codes + h * row_bytes + k * 8) = o.codes;
           p.scales_tc[sf_tc_offset(h, k, kb4)] = (uint8_t)o.sc;
+        }
+        const bool defer = live && !ok;
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, defer);
+        if (m) {
+          uint32_t base = 0;
+          if (lane == 0) base = atomicAdd(&ndef, (uint32_t)__popc(m));
+          base = __shfl_sync(0xFFFFFFFFu, base, 0);
+          const uint32_t hk = ((uint32_t)h << 16) | (uint32_t)k;
+          const uint32_t slot = base + __popc(m & ((1u << lane) - 1));
+          if (defer) {
+            if (slot < kRtDeferCta)
+              dlist[slot] = hk;
+            else
+              rt_resolve<DT>(p, alpha_d, hk, kb4);  // list full: resolve in place
+          }
         }
       }
     }
   }
+  __syncthreads();
+  const uint32_t n = min(ndef, (uint32_t)kRtDeferCta);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rt_resolve<DT>(p, alpha_d, dlist[i], kb4);
 }
 
 int g_sms[64];
@@ -278,8 +398,13 @@ int launch_status() {
 
 int check_rt(const void* a, int dtype, int groups, int64_t T, int64_t H) {
   if (!a || groups < 1 || groups > 65535 || T <= 0 || H <= 0 || (T & 15)) return F46_ERR_INVALID_ARG;
+  if (H > 65535 || (T >> 4) > 65535) return F46_ERR_UNSUPPORTED;  // deferred (h, k) packing
   if (dtype != F46_DT_BF16 && dtype != F46_DT_F32) return F46_ERR_INVALID_ARG;
   return F46_OK;
+}
+
+void fill_signs(RtParams& p) {
+  for (int i = 0; i < 16; ++i) p.sq[i] = ((p.negmask >> i) & 1u) ? -0.25f : 0.25f;
 }
 
 dim3 rt_grid(const RtParams& p, int groups) {
@@ -300,7 +425,8 @@ int f46_rht_t_amax_grouped(const void* a, int dtype, int groups, int64_t T, int6
   if (!d_amax) return F46_ERR_INVALID_ARG;
   const int64_t esz = dtype == F46_DT_BF16 ? 2 : 4;
   RtParams p{a, T, H, dtype, 0, 0, 0.0, sign_mask & 0xFFFFu, d_amax, nullptr, nullptr, nullptr,
-             nullptr, T * H * esz, 0, 0};
+             nullptr, T * H * esz, 0, 0, {}};
+  fill_signs(p);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == F46_DT_BF16)
     rht_t_amax_kernel<DT_BF16><<<rt_grid(p, groups), 256, 0, s>>>(p);
@@ -321,7 +447,8 @@ int f46_quantize_rht_t_grouped(const void* a, int dtype, int groups, int64_t T, 
   const int64_t nbT = T >> 4;
   RtParams p{a, T, H, dtype, mode, rule, mcap, sign_mask & 0xFFFFu, d_amax, codes, scales_tc,
              d_alpha_out, d_flags, T * H * esz, H * nbT * 8,
-             (int64_t)f46_scales_tc_bytes(H, T)};
+             (int64_t)f46_scales_tc_bytes(H, T), {}};
+  fill_signs(p);
   cudaStream_t s = (cudaStream_t)stream;
   const dim3 grid = rt_grid(p, groups);
 #define F46_RT_LAUNCH(DTV)                                                   \
