@@ -259,6 +259,41 @@ int f46_quantize_rht_t_grouped(const void* a, int dtype, int groups, int64_t T, 
                                double* d_amax, uint8_t* codes, uint8_t* scales_tc,
                                double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream);
 
+/*
+ * One block of any length n at any block-max target m (the reference's
+ * block-level API: compute_block_scale blockquant.py:225-236, quantize_block
+ * :379-414, quantize_block_adaptive adaptive.py:104-146 per candidate), in
+ * float64 exactly as the reference computes it.  d_x: n doubles; d_u: n
+ * uniforms for stochastic rounding or NULL for RNE; d_codes: n bytes (one code
+ * per element); d_work: n doubles (returns the dequantized block); d_out[4] =
+ * {scale code, sum diff^2, sum |diff|, max |diff|} with numpy's 1-D pairwise
+ * summation order.
+ */
+int f46_quantize_block_ref(const double* d_x, int64_t n, double alpha, double m,
+                           const double* d_u, uint8_t* d_codes, double* d_work, double* d_out,
+                           f46_stream_t stream);
+
+/*
+ * C[M,N] = A[M,K] @ B[K,N], float32, products and sums each rounded once in
+ * ascending k (no FMA): the reference's _accum_matmul_f32 (qlinear.py:64-71)
+ * bit for bit.  Used for emulated_fp4_matmul(transpose_b=False), whose B is
+ * blocked along N and so cannot feed a block-scaled tensor-core GEMM.
+ */
+int f46_matmul_f32_ordered(const float* A, const float* B, int64_t M, int64_t N, int64_t K, float* C,
+                           f46_stream_t stream);
+
+/*
+ * Test / diagnostic hooks, process-wide, default 0 (f46_runtime.h Hook):
+ *   0 SEG_CHUNK_BYTES  > 0: K2 launches at most this many input bytes at a time
+ *   1 DQ_VEC           1: dequantize takes the coalesced (non-TMA) kernel
+ *   2 Q2_V1            1: 2-D tiles take the one-tile-per-warp kernel
+ *   3 SR_ONE_THREAD    1: stochastic rounding takes the one-thread-per-block kernel
+ *   4 GEMM_KERNEL      0: CTA-pair GEMM, 1: single-CTA persistent, 2: one tile per CTA
+ * Production launches read these as plain integers; nothing is taken from
+ * the environment.
+ */
+int f46_set_test_hook(int hook, int64_t value);
+
 /* Human-readable build info ("sm_100a ..."). */
 const char* f46_build_info(void);
 

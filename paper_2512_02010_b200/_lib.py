@@ -26,6 +26,7 @@ FIXED6, FIXED4, ADAPTIVE = 0, 1, 2
 RULE = {"mse": 0, "l1": 1, "absmax": 2}
 MODE = {"fixed6": FIXED6, "fixed4": FIXED4, "adaptive": ADAPTIVE}
 SCALES_TC, SCALES_RM = 0, 1
+HOOK = {"seg_chunk_bytes": 0, "dq_vec": 1, "q2_v1": 2, "sr_one_thread": 3, "gemm_kernel": 4}
 FLAG_NONFINITE = 1
 FLAG_NAN_SCALE = 2
 
@@ -49,6 +50,9 @@ EXPORTS = (
     "f46_quantize_2d_grouped",
     "f46_rht_t_amax_grouped",
     "f46_quantize_rht_t_grouped",
+    "f46_quantize_block_ref",
+    "f46_matmul_f32_ordered",
+    "f46_set_test_hook",
     "f46_build_info",
 )
 
@@ -97,6 +101,12 @@ def _declare(L):
     L.f46_rht_t_amax_grouped.restype = i
     L.f46_quantize_rht_t_grouped.argtypes = [p, i, i, i64, i64, u32, i, i, d, p, p, p, p, p, p]
     L.f46_quantize_rht_t_grouped.restype = i
+    L.f46_quantize_block_ref.argtypes = [p, i64, d, d, p, p, p, p, p]
+    L.f46_quantize_block_ref.restype = i
+    L.f46_matmul_f32_ordered.argtypes = [p, p, i64, i64, i64, p, p]
+    L.f46_matmul_f32_ordered.restype = i
+    L.f46_set_test_hook.argtypes = [i, i64]
+    L.f46_set_test_hook.restype = i
     L.f46_build_info.argtypes = []
     L.f46_build_info.restype = ctypes.c_char_p
 

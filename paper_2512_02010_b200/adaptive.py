@@ -63,23 +63,25 @@ def quantize_tensor_adaptive(X, config: QuantConfig, alpha: Optional[float] = No
 
 def quantize_block_adaptive(block, alpha: float, rule: str = "mse", rounding: str = "rne",
                             u6=None, u4=None) -> BlockQuantResult:
-    """Adaptive quantization of one block of <= 16 values (adaptive.py:104-146)."""
+    """Adaptive quantization of one block of any length (adaptive.py:104-146):
+    both candidates in the reference's float64 arithmetic on the device, the
+    rule's error compared with a strict '<' (ties keep 6)."""
+    from .blockquant import _block_input, _block_result, _check_uniforms
+
     if rule not in _RULE_INDEX:
         raise ConfigError(f"unknown rule {rule!r}")
-    arr = as_device_tensor(block)
+    arr = _block_input(block)
     if arr.dim() != 1 or arr.numel() == 0:
         raise InvalidInputError("block must be a non-empty 1-D array")
     if not bool(torch.isfinite(arr).all()):
         raise InvalidInputError("block must be finite")
-    if rounding == "sr":
-        if u6 is None or u4 is None:
-            raise InvalidInputError("stochastic rounding requires uniforms")
-        raise ConfigError("stochastic rounding is not implemented on the B200 path yet")
-    if arr.numel() > 16:
-        raise InvalidInputError("the B200 path quantizes 16-element NVFP4 blocks")
-    q = quantize_1d(arr.reshape(1, -1), "adaptive", rule, 256.0, alpha, want_pick4=True)
-    m = 4 if int(q.pick4[0, 0].item()) else 6
-    return _block_result(arr, q, m)
+    if rounding == "sr":  # both candidates' uniforms, before any launch
+        _check_uniforms(u6, arr.numel(), "")
+        _check_uniforms(u4, arr.numel(), "")
+    cand = {m: _block_result(arr, alpha, m, u if rounding == "sr" else None)
+            for m, u in ((6.0, u6), (4.0, u4))}
+    key = {"mse": "err_mse", "l1": "err_l1", "absmax": "err_max"}[rule]
+    return cand[4.0] if getattr(cand[4.0], key) < getattr(cand[6.0], key) else cand[6.0]
 
 
 @dataclass

@@ -438,12 +438,13 @@ def quantize_tensor(X, config: QuantConfig, alpha: Optional[float] = None, sr_ta
                        rounding=config.rounding, seed=config.seed, sr_tag=sr_tag, **kw)
 
 
-def dequantize_tensor(q: QuantizedTensor, dtype: torch.dtype = torch.float32,
+def dequantize_tensor(q: QuantizedTensor, dtype: torch.dtype = torch.float64,
                       check: bool = True) -> torch.Tensor:
     """decode(code) * alpha * decode(scale) on the GPU (blockquant.py:363-376).
 
-    float64 output is the reference's exact value; float32 / bfloat16 are that
-    value rounded once.  Returns a CUDA tensor of the container's shape.
+    The default float64 output is the reference's exact value (its return
+    dtype); float32 / bfloat16 are that value rounded once (the fast paths).
+    Returns a CUDA tensor of the container's shape.
     """
     L = _lib.load()
     if q.fmt != "nvfp4":
@@ -461,42 +462,68 @@ def dequantize_tensor(q: QuantizedTensor, dtype: torch.dtype = torch.float32,
     return out.reshape(q.shape)
 
 
+def _block_input(block) -> torch.Tensor:
+    """A block for the block-level API as a torch tensor where it already is
+    (host or device): validation runs before anything is launched; the values
+    move to the device in _block_ref."""
+    if isinstance(block, torch.Tensor):
+        return block
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(block, dtype=np.float64)))
+
+
+def _block_ref(arr: torch.Tensor, alpha: float, m: float, u=None):
+    """One block through f46_quantize_block_ref: the reference's float64
+    single-block arithmetic (any length, any m) on the device.  Returns
+    (codes, scale_code, sum diff^2, sum |diff|, max |diff|, dequant)."""
+    L = _lib.load()
+    x = as_device_tensor(arr.reshape(-1).to(torch.float64)).contiguous()
+    n = x.numel()
+    dev = x.device
+    ud = None
+    if u is not None:
+        ud = as_device_tensor(np.asarray(u, dtype=np.float64).reshape(-1)).to(dev).contiguous()
+    codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    work = torch.empty(n, dtype=torch.float64, device=dev)
+    out = torch.empty(4, dtype=torch.float64, device=dev)
+    rc = L.f46_quantize_block_ref(x.data_ptr(), n, float(alpha), float(m), _lib.ptr(ud),
+                                  codes.data_ptr(), work.data_ptr(), out.data_ptr(), _stream())
+    _lib.check(rc, "f46_quantize_block_ref")
+    o = out.cpu().numpy()
+    return codes.cpu().numpy(), int(o[0]), float(o[1]), float(o[2]), float(o[3]), work.cpu().numpy()
+
+
 def compute_block_scale(block, alpha: float, m: float) -> np.uint8:
     """E4M3 code of max|block| / (alpha*m); zero blocks get code 1
-    (blockquant.py:225-236).  Runs the quantize kernel on the block."""
-    arr = as_device_tensor(block).reshape(-1)
+    (blockquant.py:225-236); any block length and target m."""
+    arr = _block_input(block).reshape(-1)
     if not bool(torch.isfinite(arr).all()):
         raise InvalidInputError("block must be finite")
     if alpha <= 0 or not np.isfinite(alpha):
         raise InvalidInputError("alpha must be positive and finite")
     if arr.numel() == 0:
         return np.uint8(1)
-    if arr.numel() > 16:
-        raise InvalidInputError("the B200 path scales 16-element NVFP4 blocks")
-    q = quantize_1d(arr.reshape(1, -1), "fixed4" if m == 4.0 else "fixed6", alpha=alpha)
-    if m not in (4.0, 6.0):
-        raise InvalidInputError("block-max target m must be 6 or 4")
-    return np.uint8(q.scale_codes[0, 0])
+    return np.uint8(_block_ref(arr, alpha, m)[1])
 
 
-def _block_result(arr: torch.Tensor, q: QuantizedTensor, m: int) -> BlockQuantResult:
+def _block_result(arr: torch.Tensor, alpha: float, m: float, u=None) -> BlockQuantResult:
+    codes, sc, ssq, sab, smx, deq = _block_ref(arr, alpha, m, u)
     n = arr.numel()
-    deq = dequantize_tensor(q, torch.float64).reshape(-1)
-    diff = deq - arr.to(torch.float64)
-    return BlockQuantResult(
-        codes=q.codes.reshape(-1),
-        scale_code=int(q.scale_codes[0, 0]),
-        chosen_m=int(m),
-        err_mse=float(torch.sum(diff * diff) / n),
-        err_l1=float(torch.sum(diff.abs()) / n),
-        err_max=float(diff.abs().max()),
-        dequant=deq.cpu().numpy(),
-    )
+    return BlockQuantResult(codes=codes, scale_code=sc, chosen_m=int(m), err_mse=ssq / n,
+                            err_l1=sab / n, err_max=smx, dequant=deq)
+
+
+def _check_uniforms(u, n: int, what: str):
+    if u is None:
+        raise InvalidInputError(f"stochastic rounding requires uniforms{what}")
+    if np.asarray(u).size != n:
+        raise InvalidInputError("u must match the block length" if what == " u" else
+                                "uniforms must match the block length")
 
 
 def quantize_block(block, alpha: float, m: float, rounding: str = "rne", u=None) -> BlockQuantResult:
-    """Quantize one block (<= 16 values) at a fixed target (blockquant.py:379-414)."""
-    arr = as_device_tensor(block)
+    """Quantize one block (any length) at a fixed target m (blockquant.py:379-414);
+    stochastic rounding takes the explicit uniforms u."""
+    arr = _block_input(block)
     if arr.dim() != 1 or arr.numel() == 0:
         raise InvalidInputError("block must be a non-empty 1-D array")
     if not bool(torch.isfinite(arr).all()):
@@ -504,15 +531,8 @@ def quantize_block(block, alpha: float, m: float, rounding: str = "rne", u=None)
     if rounding not in _ROUNDINGS:
         raise ConfigError(f"unknown rounding {rounding!r}")
     if rounding == "sr":
-        if u is None:
-            raise InvalidInputError("stochastic rounding requires uniforms u")
-        raise ConfigError("stochastic rounding is not implemented on the B200 path yet")
-    if arr.numel() > 16:
-        raise InvalidInputError("the B200 path quantizes 16-element NVFP4 blocks")
-    if m not in (4.0, 6.0):
-        raise InvalidInputError("block-max target m must be 6 or 4")
-    q = quantize_1d(arr.reshape(1, -1), "fixed4" if m == 4.0 else "fixed6", alpha=alpha)
-    return _block_result(arr, q, int(m))
+        _check_uniforms(u, arr.numel(), " u")
+    return _block_result(arr, alpha, m, u if rounding == "sr" else None)
 
 
 def reconstruction_mse(X, D) -> float:

@@ -35,6 +35,7 @@
 
 #include "../../include/fouroversix.h"
 #include "f46_ptx.cuh"
+#include "f46_runtime.h"
 
 using namespace f46::ptx;
 
@@ -1050,18 +1051,11 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   p.alpha_group_stride = alpha_per_group ? 1 : 0;
   p.c_bf16 = c_dtype == F46_DT_BF16;
   p.amax_out = amax_out;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  // CTA-pair (cta_group::2) kernel by default; F46_GEMM_1SM / F46_GEMM_SIMPLE
-  // select the single-CTA persistent / one-tile-per-CTA kernels.
-  const char* sel = getenv("F46_GEMM_KERNEL");
-  const bool want_pair = !getenv("F46_GEMM_SIMPLE") && !getenv("F46_GEMM_1SM") &&
-                         !(sel && sel[0] != 'p');
+  const int sms = f46rt::num_sms();
+  // CTA-pair (cta_group::2) kernel by default; the test hook selects the
+  // single-CTA persistent (1) or one-tile-per-CTA (2) kernels.
+  const int64_t sel = f46rt::hook(f46rt::HOOK_GEMM_KERNEL);
+  const bool want_pair = sel == 0;
   CUtensorMap msfa, msfb, mb_half, mc;
   const int esz = p.c_bf16 ? 2 : 4;
   const bool cmap = make_out_map(&mc, c, groups, M, N, ldc, esz);
@@ -1070,15 +1064,9 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
   if (want_pair && (cmap || !p.c_bf16) && make_sf_map(&msfa, a_sf, groups, p.sfa_group_stride) &&
       make_sf_map(&msfb, b_sf, groups, p.sfb_group_stride) &&
       make_code_map(&mb_half, b_codes, groups, N, kbytes, 128)) {
-    static std::once_flag pair_once;
-    std::call_once(pair_once, [] {
-      cudaFuncSetAttribute(gemm_nvfp4_pair<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes_pair<0>());
-      cudaFuncSetAttribute(gemm_nvfp4_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes_pair<1>());
-      cudaFuncSetAttribute(gemm_nvfp4_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_bytes_pair<2>());
-    });
+    f46rt::configure((const void*)gemm_nvfp4_pair<0>, smem_bytes_pair<0>(), kThreadsPair);
+    f46rt::configure((const void*)gemm_nvfp4_pair<1>, smem_bytes_pair<1>(), kThreadsPair);
+    f46rt::configure((const void*)gemm_nvfp4_pair<2>, smem_bytes_pair<2>(), kThreadsPair);
     const int64_t tiles = (int64_t)groups * ((M + 255) / 256) * ((N + BN - 1) / BN);
     const unsigned grid = 2u * (unsigned)std::min<int64_t>(tiles, sms / 2);
     if (p.c_bf16)
@@ -1095,14 +1083,9 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
     return F46_OK;
   }
   // Persistent kernel unless F46_GEMM_SIMPLE asks for the one-tile-per-CTA one.
-  if (!getenv("F46_GEMM_SIMPLE")) {
-    static std::once_flag pattr_once;
-    std::call_once(pattr_once, [] {
-      cudaFuncSetAttribute(gemm_nvfp4_persistent<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES_P);
-      cudaFuncSetAttribute(gemm_nvfp4_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SMEM_BYTES_P);
-    });
+  if (sel != 2) {
+    f46rt::configure((const void*)gemm_nvfp4_persistent<0>, SMEM_BYTES_P, kThreadsP);
+    f46rt::configure((const void*)gemm_nvfp4_persistent<1>, SMEM_BYTES_P, kThreadsP);
     const int64_t tiles = (int64_t)groups * ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
     if (p.c_bf16)
@@ -1117,13 +1100,8 @@ int gemm_launch(int groups, const uint8_t* a_codes, const uint8_t* a_sf, const d
     return F46_OK;
   }
   const dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM), (unsigned)groups);
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(gemm_nvfp4_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    cudaFuncSetAttribute(gemm_nvfp4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-  });
+  f46rt::configure((const void*)gemm_nvfp4_kernel<0>, SMEM_BYTES, kThreads);
+  f46rt::configure((const void*)gemm_nvfp4_kernel<1>, SMEM_BYTES, kThreads);
   if (p.c_bf16)
     gemm_nvfp4_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ma, mb, p);
   else

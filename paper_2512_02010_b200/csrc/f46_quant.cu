@@ -30,6 +30,7 @@
 
 #include "../../include/fouroversix.h"
 #include "f46_device.cuh"
+#include "f46_runtime.h"
 
 using namespace f46;
 
@@ -40,17 +41,7 @@ namespace {
 #endif
 constexpr int kStages = F46_STAGES;
 
-int g_num_sms = 0;
-
-int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
+int num_sms() { return f46rt::num_sms(); }
 
 // ---------------------------------------------------------------------------
 // mbarrier / TMA helpers
@@ -1914,6 +1905,111 @@ __global__ void __launch_bounds__(256, 3) quant_sr4_kernel(SRParams sp) {
   if (nonfinite && lane == 0 && p.d_flags) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
 }
 
+// ---------------------------------------------------------------------------
+// Single block of any length at any target m (the reference's block-level API,
+// blockquant.py:225-236 compute_block_scale and :379-414 quantize_block): one
+// thread restates the float64 arithmetic, including numpy's 1-D pairwise sum
+// for the error means (n < 8: sequential from -0.0; n <= 128: 8 accumulators
+// + tail; larger: split at n/2 rounded down to a multiple of 8).
+// ---------------------------------------------------------------------------
+__device__ double np_pairwise_sum(const double* a, int64_t n, int kind) {
+  // kind 0: a[i]^2 of the diffs, 1: |a[i]|
+  auto term = [&](int64_t i) -> double { return kind == 0 ? __dmul_rn(a[i], a[i]) : fabs(a[i]); };
+  if (n < 8) {
+    double res = -0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, term(i));
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = term(j);
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], term(i + j));
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, term(i));
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2, kind), np_pairwise_sum(a + n2, n - n2, kind));
+}
+
+// x: n float64 values; u: n uniforms (stochastic rounding) or null (RNE).
+// Writes codes[n], work[n] (the diffs, then overwritten with deq), and
+// out[4] = {scale code, sum diff^2, sum |diff|, max |diff|}.
+__global__ void block_ref_kernel(const double* __restrict__ x, int64_t n, double alpha, double m,
+                                 const double* __restrict__ u, uint8_t* __restrict__ codes,
+                                 double* __restrict__ work, double* __restrict__ out) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double bmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) bmax = fmax(bmax, fabs(x[i]));
+  // _nvfp4_scales (blockquant.py:239-242)
+  uint32_t sc = enc_e4m3_d(__ddiv_rn(bmax, __dmul_rn(alpha, m)));
+  if (bmax == 0.0) sc = 1;
+  const double denom = __dmul_rn(alpha, dec_e4m3_d(sc));
+  double mx = 0.0;
+  // _cast_values (blockquant.py:260-280)
+  for (int64_t i = 0; i < n; ++i) {
+    double s;
+    if (denom > 0.0)
+      s = __ddiv_rn(x[i], denom);
+    else
+      s = (x[i] != 0.0) ? copysign(6.0, x[i]) : 0.0;
+    const uint32_t c = u ? enc_fp4_sr_d(s, u[i]) : enc_fp4_d(s);
+    codes[i] = (uint8_t)c;
+    const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(c), denom), x[i]);
+    work[i] = diff;
+    mx = fmax(mx, fabs(diff));
+  }
+  out[0] = (double)sc;
+  out[1] = np_pairwise_sum(work, n, 0);
+  out[2] = np_pairwise_sum(work, n, 1);
+  out[3] = mx;
+  for (int64_t i = 0; i < n; ++i) work[i] = __dmul_rn(dec_fp4_d(codes[i]), denom);
+}
+
+// ---------------------------------------------------------------------------
+// qlinear.py:64-71 _accum_matmul_f32 restated: C = A @ B with float32 products
+// summed in ascending k, one rounding each (no FMA): the reference's
+// emulated_fp4_matmul for operands it cannot hand to a block-scaled tensor-core
+// instruction (transpose_b=False: B blocked along N).  A [M,K], B [K,N], C
+// [M,N] row-major float32; 32x32 output tiles staged through shared memory
+// in ascending k.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) matmul_f32_ordered_kernel(const float* __restrict__ A,
+                                                                const float* __restrict__ B,
+                                                                int64_t M, int64_t N, int64_t K,
+                                                                float* __restrict__ C) {
+  __shared__ float As[32][33], Bs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads, 4 rows each
+  const int64_t n = (int64_t)blockIdx.x * 32 + tx;
+  const int64_t m0 = (int64_t)blockIdx.y * 32;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t k0 = 0; k0 < K; k0 += 32) {
+    for (int r = ty; r < 32; r += 8) {
+      const int64_t m = m0 + r, k = k0 + tx;
+      As[r][tx] = (m < M && k < K) ? A[m * K + k] : 0.f;
+      const int64_t kb = k0 + r;
+      Bs[r][tx] = (kb < K && n < N) ? B[kb * N + n] : 0.f;
+    }
+    __syncthreads();
+    const int kt = (K - k0) < 32 ? (int)(K - k0) : 32;
+    for (int kk = 0; kk < kt; ++kk) {
+      const float b = Bs[kk][tx];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = __fadd_rn(acc[i], __fmul_rn(As[ty + 8 * i][kk], b));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + ty + 8 * i;
+    if (m < M && n < N) C[m * N + n] = acc[i];
+  }
+}
+
 // transforms.py:92-97 apply_rht: y = fwht(g * signs) / sqrt(16) per group of
 // 16 along the last dim, float64, numpy's butterfly order (h = 1, 2, 4, 8).
 template <int DT>
@@ -2634,25 +2730,15 @@ template <int DT, int MODE, bool EXTRA>
 int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
   constexpr int kTileBytes = kSegElems * ((DT == DT_BF16) ? 2 : 4);
   const int smem = kWarps * kStages * kTileBytes;
-  static bool configured = false;
-  static int ctas_per_sm = 1;
-  if (!configured) {
-    cudaFuncSetAttribute(quant_seg_kernel<DT, MODE, EXTRA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quant_seg_kernel<DT, MODE, EXTRA>,
-                                                  kWarps * 32, smem);
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-    configured = true;
-  }
+  const int ctas_per_sm =
+      f46rt::configure((const void*)quant_seg_kernel<DT, MODE, EXTRA>, smem, kWarps * 32);
   // The kernel keeps 32-bit byte offsets: launch at most 2^31 input bytes at a
   // time, in whole 128-row slabs so each launch owns complete scale atoms.
   constexpr int64_t kEsz = (DT == DT_BF16) ? 2 : 4;
   const int64_t nb = p.cols >> 4, kb4 = (nb + 3) >> 2;
   int64_t chunk_bytes = (int64_t)1 << 31;
-  if (const char* e = getenv("F46_SEG_CHUNK_BYTES")) {  // test hook: force multi-launch
-    const long long v = atoll(e);
-    if (v > 0 && v < chunk_bytes) chunk_bytes = v;
-  }
+  const int64_t hook_bytes = f46rt::hook(f46rt::HOOK_SEG_CHUNK_BYTES);  // test hook: force multi-launch
+  if (hook_bytes > 0 && hook_bytes < chunk_bytes) chunk_bytes = hook_bytes;
   int64_t rows_max = (chunk_bytes / (p.cols * kEsz)) & ~(int64_t)127;
   if (rows_max < 128) return F46_ERR_UNSUPPORTED;
   if (groups > 1) {  // one launch, group = blockIdx.y; each group within one slab
@@ -2717,14 +2803,8 @@ int launch_dequant_tma_t(const CUtensorMap& map, const uint8_t* codes, const uin
                          const double* d_alpha, const DqArgs& a, void* out, uint32_t* d_flags,
                          cudaStream_t s) {
   using C = DqTma<OUT>;
-  static int ctas_per_sm = 0;
-  if (ctas_per_sm == 0) {
-    cudaFuncSetAttribute(dequant_tma_kernel<OUT, SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, dequant_tma_kernel<OUT, SL>,
-                                                  C::kWarpsPerCta * 32, C::kSmem);
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-  }
+  const int ctas_per_sm =
+      f46rt::configure((const void*)dequant_tma_kernel<OUT, SL>, C::kSmem, C::kWarpsPerCta * 32);
   const int64_t nsup = (a.n + (int64_t)C::kChunk * C::kU - 1) / ((int64_t)C::kChunk * C::kU);
   int64_t grid = (nsup + C::kWarpsPerCta - 1) / C::kWarpsPerCta;
   const int64_t cap = (int64_t)num_sms() * ctas_per_sm;
@@ -2782,10 +2862,23 @@ int launch_dequant_tma(const uint8_t* codes, const uint8_t* scales, bool tc, con
 
 }  // namespace
 
+namespace f46rt {
+namespace {
+std::atomic<int64_t> g_hooks[HOOK_COUNT];
+}
+int64_t hook(int h) { return (h >= 0 && h < HOOK_COUNT) ? g_hooks[h].load(std::memory_order_relaxed) : 0; }
+}  // namespace f46rt
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" {
+
+int f46_set_test_hook(int hook, int64_t value) {
+  if (hook < 0 || hook >= f46rt::HOOK_COUNT) return F46_ERR_INVALID_ARG;
+  f46rt::g_hooks[hook].store(value, std::memory_order_relaxed);
+  return F46_OK;
+}
 
 size_t f46_scales_tc_bytes(int64_t rows, int64_t cols) {
   const int64_t nb = (cols + 15) / 16;
@@ -2944,6 +3037,23 @@ int f46_quantize_2d_grouped(const void* w, int dtype, int groups, int64_t R, int
   return launch_status();
 }
 
+int f46_matmul_f32_ordered(const float* A, const float* B, int64_t M, int64_t N, int64_t K, float* C,
+                           f46_stream_t stream) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0) return F46_ERR_INVALID_ARG;
+  if ((N + 31) / 32 > 0x7FFFFFFF || (M + 31) / 32 > 65535) return F46_ERR_UNSUPPORTED;
+  const dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
+  matmul_f32_ordered_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, B, M, N, K, C);
+  return launch_status();
+}
+
+int f46_quantize_block_ref(const double* d_x, int64_t n, double alpha, double m,
+                           const double* d_u, uint8_t* d_codes, double* d_work, double* d_out,
+                           f46_stream_t stream) {
+  if (!d_x || !d_codes || !d_work || !d_out || n <= 0) return F46_ERR_INVALID_ARG;
+  block_ref_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(d_x, n, alpha, m, d_u, d_codes, d_work, d_out);
+  return launch_status();
+}
+
 int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout,
                    const double* d_alpha, int64_t rows, int64_t cols, void* out, int out_dtype,
                    uint32_t* d_flags, f46_stream_t stream) {
@@ -2957,7 +3067,7 @@ int f46_dequantize(const uint8_t* codes, const uint8_t* scales, int scale_layout
   const bool tc = scale_layout == F46_SCALES_TC;
   // TMA-staged path: f32 / bf16 out, cols % 16 == 0, 16-byte aligned codes and output
   if ((out_dtype == F46_DT_F32 || out_dtype == F46_DT_BF16) && cols % 16 == 0 &&
-      (((uintptr_t)out) & 15) == 0 && (((uintptr_t)codes) & 15) == 0 && !getenv("F46_DQ_VEC")) {
+      (((uintptr_t)out) & 15) == 0 && (((uintptr_t)codes) & 15) == 0 && !f46rt::hook(f46rt::HOOK_DQ_VEC)) {
     const int rc = launch_dequant_tma(codes, scales, tc, d_alpha, rows, cols, out, out_dtype, d_flags, s);
     if (rc != F46_ERR_UNSUPPORTED) return rc;
   }
@@ -3016,7 +3126,7 @@ int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, in
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  if (dtype != F46_DT_F64 && !getenv("F46_Q2_V1")) {
+  if (dtype != F46_DT_F64 && !f46rt::hook(f46rt::HOOK_Q2_V1)) {
     int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
     const int64_t cap2 = (int64_t)num_sms() * 8;
     if (g2 > cap2) g2 = cap2;
@@ -3074,7 +3184,7 @@ int f46_quantize_sr(const void* x, int dtype, int64_t rows, int64_t cols, int mo
   int64_t grid = (total + 127) / 128;
   const int64_t cap = (int64_t)num_sms() * 16;
   if (grid > cap) grid = cap;
-  const bool quad = !getenv("F46_SR_ONE_THREAD");
+  const bool quad = !f46rt::hook(f46rt::HOOK_SR_ONE_THREAD);
   int64_t grid4 = (total * 4 + 255) / 256;
   const int64_t cap4 = (int64_t)num_sms() * 8;
   if (grid4 > cap4) grid4 = cap4;

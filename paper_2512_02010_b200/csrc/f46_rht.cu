@@ -25,6 +25,7 @@
 
 #include "../../include/fouroversix.h"
 #include "f46_device.cuh"
+#include "f46_runtime.h"
 
 using namespace f46;
 
@@ -373,19 +374,7 @@ __global__ void __launch_bounds__(256, F46_RT_MINB) quant_rht_t_kernel(RtParams 
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) rt_resolve<DT>(p, alpha_d, dlist[i], kb4);
 }
 
-int g_sms[64];
-
-int num_sms() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (g_sms[dev] == 0) {
-    int n = 0;
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    g_sms[dev] = n > 0 ? n : 148;
-  }
-  return g_sms[dev];
-}
+int num_sms() { return f46rt::num_sms(); }
 
 int launch_status() {
   const cudaError_t e = cudaGetLastError();

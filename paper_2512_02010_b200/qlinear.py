@@ -15,8 +15,10 @@ order, so results agree to float32 accumulation error (relative Frobenius
 
 ``transpose_b=False`` asks for dequant(A) @ dequant(B) with B blocked along N,
 which no block-scaled tensor-core instruction can consume; that case
-dequantizes both operands exactly on the GPU (f46_dequantize) and multiplies
-in float32 with TF32 disabled.
+dequantizes both operands on the GPU (f46_dequantize, rounded once to
+float32 as the reference's ``astype(np.float32)``) and runs the reference's
+ordered float32 accumulation (f46_matmul_f32_ordered) -- bit-identical to
+``_accum_matmul_f32``.
 """
 
 from __future__ import annotations
@@ -125,14 +127,16 @@ def emulated_fp4_matmul(aq: QuantizedTensor, bq: QuantizedTensor, *, transpose_b
         return gemm_nvfp4(aq, bq, torch.float32)
     if aq.shape[1] != bq.shape[0]:
         raise InvalidInputError(f"inner dimensions differ: {aq.shape} x {bq.shape}")
-    A = dequantize_tensor(aq, torch.float32)
-    B = dequantize_tensor(bq, torch.float32)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        C = A @ B
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    # the reference's own arithmetic: operands rounded once to float32, float32
+    # products summed in ascending k (bit-identical to _accum_matmul_f32)
+    A = dequantize_tensor(aq, torch.float32).contiguous()
+    B = dequantize_tensor(bq, torch.float32).contiguous()
+    M, K = A.shape
+    N = B.shape[1]
+    C = torch.empty((M, N), dtype=torch.float32, device=A.device)
+    L = _lib.load()
+    _lib.check(L.f46_matmul_f32_ordered(A.data_ptr(), B.data_ptr(), M, N, K, C.data_ptr(), _stream()),
+               "f46_matmul_f32_ordered")
     return round_to_bf16(C) if bf16_out else C
 
 

@@ -21,3 +21,21 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture
+def test_hook():
+    """Set a library test hook (f46_set_test_hook) for one test; every hook
+    set through it is reset to 0 afterwards."""
+    from paper_2512_02010_b200 import _lib
+
+    L = _lib.load()
+    used = set()
+
+    def set_hook(name, value):
+        used.add(name)
+        assert L.f46_set_test_hook(_lib.HOOK[name], int(value)) == 0
+
+    yield set_hook
+    for name in used:
+        L.f46_set_test_hook(_lib.HOOK[name], 0)

@@ -334,6 +334,71 @@ def sr_rht_cases():
     print(f"wrote {len(names)} sr/rht cases to {path}")
 
 
+def block_api_cases():
+    """The block-level API at any length and target (blockquant.py:225-236
+    compute_block_scale, :379-414 quantize_block incl. stochastic rounding
+    with explicit uniforms, adaptive.py:104-146 quantize_block_adaptive per
+    rule) and emulated_fp4_matmul with transpose_b=False (qlinear.py:74-93,
+    the ordered float32 accumulation)."""
+    out, names = {}, []
+
+    def put(name, **rec):
+        names.append(name)
+        for k, v in rec.items():
+            out[f"{name}::{k}"] = v
+
+    rng = philox(1500)
+    lengths = (1, 3, 7, 8, 13, 16, 17, 33, 129, 300)
+    for i, n in enumerate(lengths):
+        x = rng.standard_normal(n) * np.exp(rng.standard_normal() * 2)
+        if i == 2:
+            x[1] = -0.0
+        alpha = float(np.float32(np.max(np.abs(x)) / 1536.0)) * (1.0 + 2.0 ** -20 * i)
+        u = rng.random(n)
+        for m in (6.0, 4.0, 5.5, 3.0):
+            for rounding in ("rne", "sr"):
+                r = ref_bq.quantize_block(x, alpha, m, rounding=rounding, u=u if rounding == "sr" else None)
+                put(f"qb_n{n}_m{m}_{rounding}", x=x, alpha=np.array(alpha), m=np.array(m),
+                    rounding=np.array(rounding), u=u, codes=np.asarray(r.codes, np.uint8),
+                    scale=np.array(r.scale_code), err=np.array([r.err_mse, r.err_l1, r.err_max]),
+                    deq=np.asarray(r.dequant, np.float64),
+                    cbs=np.array(int(ref_bq.compute_block_scale(x, alpha, m))))
+        u4 = rng.random(n)
+        for rule in ("mse", "l1", "absmax"):
+            for rounding in ("rne", "sr"):
+                r = ref_adaptive.quantize_block_adaptive(x, alpha, rule=rule, rounding=rounding,
+                                                         u6=u if rounding == "sr" else None,
+                                                         u4=u4 if rounding == "sr" else None)
+                put(f"qba_n{n}_{rule}_{rounding}", x=x, alpha=np.array(alpha), rule=np.array(rule),
+                    rounding=np.array(rounding), u6=u, u4=u4, codes=np.asarray(r.codes, np.uint8),
+                    scale=np.array(r.scale_code), m=np.array(r.chosen_m),
+                    err=np.array([r.err_mse, r.err_l1, r.err_max]))
+    # Table-2 blocks at alpha = 1 (test_acceptance.py:46-75)
+    for name, blk in (("A", [10.0, 20.0, 30.0, 40.0]), ("B", [15.0, 30.0, 120.0, 180.0])):
+        for m in (6.0, 4.0):
+            r = ref_bq.quantize_block(np.array(blk), 1.0, m)
+            put(f"table2_{name}_m{m}", x=np.array(blk), alpha=np.array(1.0), m=np.array(m),
+                rounding=np.array("rne"), u=np.zeros(4), codes=np.asarray(r.codes, np.uint8),
+                scale=np.array(r.scale_code), err=np.array([r.err_mse, r.err_l1, r.err_max]),
+                deq=np.asarray(r.dequant, np.float64),
+                cbs=np.array(int(ref_bq.compute_block_scale(np.array(blk), 1.0, m))))
+    # transpose_b=False: A [M,K] blocked along K, B [K,N] blocked along N
+    for i, (M, K, N) in enumerate([(24, 64, 40), (17, 48, 33)]):
+        a = bf16_to_f64(bf16(philox(1600 + i).standard_normal((M, K))))
+        b = bf16_to_f64(bf16(philox(1650 + i).standard_normal((K, N)) * 0.3))
+        cfg = fp4emu.QuantConfig(scale_mode="adaptive")
+        aq = fp4emu.quantize_tensor_adaptive(a, cfg)
+        bq = fp4emu.quantize_tensor_adaptive(b, cfg)
+        c = fp4emu.emulated_fp4_matmul(aq, bq, transpose_b=False)
+        c16 = fp4emu.emulated_fp4_matmul(aq, bq, transpose_b=False, bf16_out=True)
+        put(f"mm_nn_{M}x{K}x{N}", a=bf16_bits(a.astype(np.float32)), b=bf16_bits(b.astype(np.float32)),
+            c=np.asarray(c, np.float32), c16=np.asarray(c16, np.float32))
+    out["__names__"] = np.array(names)
+    path = os.path.join(HERE, "golden_block.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {len(names)} block-api cases to {path}")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "sr":
         sr_rht_cases()
@@ -341,8 +406,11 @@ if __name__ == "__main__":
         linear_cases()
     elif len(sys.argv) > 1 and sys.argv[1] == "io":
         io_and_stats_cases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "block":
+        block_api_cases()
     else:
         main()
         linear_cases()
         io_and_stats_cases()
         sr_rht_cases()
+        block_api_cases()

@@ -91,7 +91,7 @@ def test_dequant_routes_agree(shape, dtype):
 
 
 @pytest.mark.parametrize("mode", ["adaptive", "fixed6", "fixed4"])
-def test_tile2d_v2_special_tiles_equal_v1(mode, monkeypatch):
+def test_tile2d_v2_special_tiles_equal_v1(mode, test_hook):
     """The two-tiles-per-warp 2-D kernel against the one-tile-per-warp kernel
     on all-zero tiles (with -0.0), tiles beyond the fast path's magnitude
     range (float32 input, 1e30) and ragged edges."""
@@ -104,9 +104,9 @@ def test_tile2d_v2_special_tiles_equal_v1(mode, monkeypatch):
     for t in (x.float(), x.to(torch.bfloat16)):
         cfg = f46.QuantConfig(scale_mode=mode)
         a = f46.quantize_weights_2d(t.cuda(), cfg, want_rowmajor=True)
-        monkeypatch.setenv("F46_Q2_V1", "1")
+        test_hook("q2_v1", 1)
         b = f46.quantize_weights_2d(t.cuda(), cfg, want_rowmajor=True)
-        monkeypatch.delenv("F46_Q2_V1")
+        test_hook("q2_v1", 0)
         same(a, b)
         same(a.transposed, b.transposed)
         assert torch.equal(a.scales_rm, b.scales_rm)

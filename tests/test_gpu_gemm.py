@@ -146,9 +146,9 @@ def test_grouped_matches_per_group():
 
 
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
-def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
+def test_persistent_and_simple_kernels_agree(out_dtype, test_hook):
     """The CTA-pair kernel (default), the single-CTA persistent kernel
-    (F46_GEMM_1SM) and the one-tile-per-CTA kernel (F46_GEMM_SIMPLE) accumulate
+    (test hook gemm_kernel 1) and the one-tile-per-CTA kernel (gemm_kernel 2) accumulate
     every output element over K in the same order: identical bits, also into
     a strided output (ldc = N + 1)."""
     M, N, K = 700, 1000, 1024
@@ -157,9 +157,9 @@ def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
     fast = f46.gemm_nvfp4(aq, bq, out_dtype)
     wide = torch.empty((M, N + 1), dtype=out_dtype, device="cuda")
     strided = f46.gemm_nvfp4(aq, bq, out_dtype, out=wide[:, :N])
-    monkeypatch.setenv("F46_GEMM_1SM", "1")
+    test_hook("gemm_kernel", 1)
     one_sm = f46.gemm_nvfp4(aq, bq, out_dtype)
-    monkeypatch.setenv("F46_GEMM_SIMPLE", "1")
+    test_hook("gemm_kernel", 2)
     simple = f46.gemm_nvfp4(aq, bq, out_dtype)
     assert torch.equal(one_sm, simple)
     assert torch.equal(fast, strided)
@@ -170,14 +170,11 @@ def test_persistent_and_simple_kernels_agree(out_dtype, monkeypatch):
 @pytest.mark.parametrize("kernel", ["pair", "1sm", "simple"])
 @pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("M,N,K", [(700, 1000, 1024), (256, 512, 256), (33, 40, 48)])
-def test_producer_fused_amax(M, N, K, out_dtype, kernel, monkeypatch):
+def test_producer_fused_amax(M, N, K, out_dtype, kernel, test_hook):
     """The epilogue's amax equals max |C| of the stored tensor exactly (every
     kernel, every output type, ragged tiles) and, handed to the next quantize
     as its amax, yields the container K1 + K2 produce."""
-    if kernel == "1sm":
-        monkeypatch.setenv("F46_GEMM_1SM", "1")
-    elif kernel == "simple":
-        monkeypatch.setenv("F46_GEMM_SIMPLE", "1")
+    test_hook("gemm_kernel", {"pair": 0, "1sm": 1, "simple": 2}[kernel])
     aq = f46.quantize_tensor_adaptive(bf16_randn((M, K), 81).cuda(), ADAPT)
     bq = f46.quantize_tensor_adaptive(bf16_randn((N, K), 82).cuda(), ADAPT)
     amax = torch.full((1,), 123.0, dtype=torch.float64, device="cuda")  # zeroed by the call

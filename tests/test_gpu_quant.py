@@ -178,13 +178,13 @@ def test_reference_style_float64_inputs():
 @pytest.mark.parametrize("shape", [(5, 48), (1, 16), (3, 1040), (33, 4112), (64, 1024), (257, 2064),
                                    (130, 272)])
 @pytest.mark.parametrize("path", ["tma", "vec"])
-def test_dequant_flat_paths_ragged(shape, alpha, path, monkeypatch):
+def test_dequant_flat_paths_ragged(shape, alpha, path, test_hook):
     """K3's TMA-staged and coalesced variants on chunk- and row-ragged shapes
     (odd blocks per row too), with f32-exact alphas (direct and round-to-odd
     bf16 routes) and an f64-only alpha: f32 is the exact value rounded once,
     bf16 likewise (a single rounding of the float64 value)."""
     if path == "vec":
-        monkeypatch.setenv("F46_DQ_VEC", "1")
+        test_hook("dq_vec", 1)
     x = bf16_randn(shape, shape[0] * 31 + shape[1])
     q = run(x.cuda(), "adaptive", alpha=alpha)
     d64 = f46.dequantize_tensor(q, torch.float64).cpu().numpy()
@@ -195,13 +195,13 @@ def test_dequant_flat_paths_ragged(shape, alpha, path, monkeypatch):
 
 
 @pytest.mark.parametrize("mode", ["adaptive", "fixed6"])
-def test_k2_multi_launch_row_slabs(mode, monkeypatch):
+def test_k2_multi_launch_row_slabs(mode, test_hook):
     """K2 keeps 32-bit offsets and launches at most 2^31 input bytes at a time
     in 128-row slabs; forcing 1 MB slabs (4 launches + a ragged last slab)
     gives the single-launch container bit for bit."""
     x = bf16_randn((1000, 512), 5).cuda()
     ref = run(x, mode)
-    monkeypatch.setenv("F46_SEG_CHUNK_BYTES", str(1 << 18))
+    test_hook("seg_chunk_bytes", 1 << 18)
     got = run(x, mode)
     assert got.alpha == ref.alpha
     assert torch.equal(got.packed_codes, ref.packed_codes)

@@ -10,6 +10,8 @@ from paper_2512_02010_b200.blockquant import scales_tc_bytes
 
 rows, cols = 65536, 4096
 L = _lib.load()
+if os.environ.get("F46_DQ_VEC"):  # tool-side switch onto the library test hook
+    L.f46_set_test_hook(1, 1)
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(5)
 codes = torch.randint(0, 256, (rows, cols // 2), generator=g, device=dev, dtype=torch.uint8)
