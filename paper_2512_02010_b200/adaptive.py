@@ -98,7 +98,11 @@ def selection_stats(X, config: QuantConfig, alpha: Optional[float] = None,
                     sr_tag: int = 0) -> SelectionStats:
     """Per-rule selection statistics (adaptive.py:159-187) from one fused
     device pass (f46_selection_stats: exact float64 errors of both candidates,
-    all three rules' picks, counts and chosen squared errors per block)."""
+    all three rules' picks, counts and chosen squared errors per block).
+    fraction_4 and disagreements are exact counts; aggregate_mse sums the exact
+    per-block errors in a fixed device order (per thread, then per CTA part,
+    then the parts), so it equals the reference's numpy sum to float64
+    rounding, not bit for bit."""
     from . import _lib
     from .blockquant import _DT_OF, _check_alpha_override, _stream, _validated_shape, amax_device
 
@@ -110,12 +114,14 @@ def selection_stats(X, config: QuantConfig, alpha: Optional[float] = None,
     t = as_device_tensor(X)
     rows, cols = _validated_shape(t)
     a_over, d_amax = 0.0, None
+    # the reference validates X before anything else (_validated, blockquant.py:191-199):
+    # one device max|X| doubles as the finiteness check, with or without an override
+    d_amax = amax_device(t)
+    if not bool(torch.isfinite(d_amax).all()):
+        raise InvalidInputError("tensor must be finite")
     if alpha is not None:
         a_over = _check_alpha_override(alpha)
-    else:
-        d_amax = amax_device(t)
-        if not bool(torch.isfinite(d_amax).all()):
-            raise InvalidInputError("tensor must be finite")
+        d_amax = None
     nparts = 4 * torch.cuda.get_device_properties(t.device).multi_processor_count
     parts = torch.empty((nparts, 9), dtype=torch.float64, device=t.device)
     rc = L.f46_selection_stats(t.data_ptr(), _DT_OF[t.dtype], rows, cols, 1536.0,

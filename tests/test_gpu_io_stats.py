@@ -84,3 +84,28 @@ def test_selection_stats_fast_path_matches_float64_path():
     assert a.fraction_4 == b.fraction_4
     assert a.disagreements == b.disagreements
     assert a.aggregate_mse == b.aggregate_mse
+
+
+def test_selection_stats_rejects_nonfinite_with_alpha_override():
+    x = torch.randn(32, 64).to(torch.bfloat16)
+    x[3, 3] = float("nan")
+    with pytest.raises(f46.InvalidInputError):
+        f46.selection_stats(x.cuda(), f46.QuantConfig(scale_mode="adaptive"), alpha=0.01)
+
+
+def test_reader_errors(tmp_path):
+    p = tmp_path / "bad.nvf4"
+    p.write_bytes(b"XXXX")
+    with pytest.raises(f46.BadMagicError):
+        f46.read_quantized(p)
+    p.write_bytes(b"NVF4\x00")
+    with pytest.raises(f46.TruncatedFileError):
+        f46.read_quantized(p)
+    p.write_bytes(b"NVF4\x07\x01" + (16).to_bytes(8, "little"))
+    with pytest.raises(f46.UnsupportedDtypeError):
+        f46.read_quantized(p)
+    q = f46.quantize_tensor_adaptive(torch.randn(4, 16).cuda(), f46.QuantConfig(scale_mode="adaptive"))
+    f46.write_quantized(p, q)
+    p.write_bytes(p.read_bytes() + b"\x00")
+    with pytest.raises(f46.FormatError):
+        f46.read_quantized(p)
