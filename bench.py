@@ -809,12 +809,33 @@ def bench_moe(args, dev):
         tot_flops += fl
         gemm_ms += ms
     step_ms = timed_back_to_back(lambda: moe_step(t, cfg), stream, 3, warm=1)
+    # the quantize half by operand kind, each one grouped call over the 16
+    # experts (amax pass + quantize pass), L2 flushed, bytes = algorithmic
+    # HBM traffic of both passes
+    peaks, _ = measured_peaks()
+    flush = L2Flush(dev)
+    spec = f46.RhtSpec(seed=cfg.seed)
+    kinds = {
+        "x_1d": (lambda: f46.quantize_grouped(t["x"], cfg, check_finite=False), t["x"].numel(), 4.5625),
+        "h_1d": (lambda: f46.quantize_grouped(t["h"], cfg, check_finite=False), t["h"].numel(), 4.5625),
+        "w1_2d_w_and_wt": (lambda: f46.quantize_weights_2d_grouped(t["W1"], cfg, check_finite=False),
+                           t["W1"].numel(), 2 * 2 + 2 * 0.5625),
+        "dy_wgrad_rht_t": (lambda: f46.quantize_wgrad_operand_grouped(t["dy"], cfg, spec, check_finite=False),
+                           t["dy"].numel(), 4.5625),
+    }
+    qk = {}
+    for name, (fn, n, bpe) in kinds.items():
+        ms = timed_flushed(fn, flush, stream, 10)
+        qk[name] = {"ms": ms, "GB/s": n * bpe / ms / 1e6, "frac_of_hbm": n * bpe / ms / 1e6 / peaks["hbm_gbs"],
+                    "bytes_per_elem": bpe}
     return {"per_gemm": res, "gemm_TFLOP/s": tot_flops / (gemm_ms * 1e-3) / 1e12, "gemm_ms": gemm_ms,
             "step_ms": step_ms, "quantize_ms": step_ms - gemm_ms,
             "step_TFLOP/s": tot_flops / (step_ms * 1e-3) / 1e12,
+            "quantize_by_kind": qk,
             "note": ("per GPU of EP=8: 8 GPUs x 8192 tokens x top-6 / 128 experts = 3072 tokens/expert; "
-                     "step = quantize all operands (public API, per expert) + 6 grouped GEMMs, "
-                     "rounding rne (the QuantConfig default)")}
+                     "step = quantize all operands (one grouped launch pair per operand: X, H, dY, dH 1-D; "
+                     "W1, W2 2-D tiles with W^T; dY, H, dH, X transposed through the RHT for WGRAD; each "
+                     "expert its own tensor scale) + 6 grouped GEMMs, rounding rne (the QuantConfig default)")}
 
 
 def cpu_baseline(args):

@@ -766,6 +766,62 @@ __device__ __forceinline__ float4 scale_entry(uint32_t c, float alpha) {
   return e;
 }
 
+// The E4M3 code of bmax/(alpha*m) when the bracket gave lo and lo + 1: the
+// tie T between them (5 significant bits, T*m exact in f32) decides with one
+// correctly rounded fma; an exact tie goes to the even code (codecs.py:158-178).
+__device__ __forceinline__ uint32_t scale_tie(uint32_t lo, float bmax, float alpha, float m) {
+  const float T = 0.5f * (e4m3_to_f32(lo) + e4m3_to_f32(lo + 1));
+  const float s = fmaf(alpha, T * m, -bmax);
+  return s > 0.f ? lo : (s < 0.f ? lo + 1 : ((lo & 1u) ? lo + 1 : lo));
+}
+
+// True when bmax/(alpha*m) can land exactly on an E4M3 tie for a BF16 bmax:
+// bmax = alpha * m * T needs odd(alpha) * odd(m) * odd(T) <= 255 with odd(T)
+// >= 17 (a tie between two 4-bit significands has 5), i.e. odd(alpha) <= 15.
+// Only tensors whose alpha has that few significant bits need block46's
+// in-place tie resolution; the rest keep the leaner straight line.
+__device__ __forceinline__ bool e4m3_ties_possible(float alpha) {
+  const uint32_t sig = (__float_as_uint(alpha) & 0x7FFFFFu) | 0x800000u;
+  return (sig >> (__ffs(sig) - 1)) <= 15u;
+}
+
+// TDIR 0 (alpha = amax / mcap exactly, so D = alpha * E4M3(c) is exact and
+// every near-tie quotient is an exact FP4 tie, tie_direction()): look for a
+// reciprocal R of D, within 4 ulps of RN(1/D), such that for every tie t whose
+// value t*D is a BF16 number (the only ties an element can hit) cvt.rn of
+// RN(t*D*R) gives the reference's code (ties to even).  Non-tie quotients lie
+// >= 2^-16.3 (relative) from every tie and x*R is within 2^-20.5 of x/D, so
+// with such an R the codes of x*R are the reference's for every element: the
+// candidate pass can keep its codes with no upper-bound pass.  Returns false
+// when no such R exists (then the tensor keeps the two-bound TDIR 0 path).
+__device__ __forceinline__ bool safe_recip(uint32_t c, float alpha, float& R) {
+  const float D = alpha * e4m3_to_f32(c);
+  if (!(D > 0.f) || !(D < 1e30f)) return false;
+  const float R0 = __frcp_rn(D);
+  // the ties' reference codes (RNE on the code index): 0.25->0 .75->2 1.25->2
+  // 1.75->4 2.5->4 3.5->6 5->6
+  const float ties[7] = {0.25f, 0.75f, 1.25f, 1.75f, 2.5f, 3.5f, 5.f};
+  const uint32_t want[7] = {0, 2, 2, 4, 4, 6, 6};
+#pragma unroll 1
+  for (int s = 0; s < 9; ++s) {
+    const int k = (s & 1) ? (s + 1) / 2 : -(s / 2);  // 0, 1, -1, 2, -2, ...
+    const float r = __int_as_float(__float_as_int(R0) + k);
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      const float x = ties[i] * D;  // exact: <= 3 + 12 significant bits
+      if ((__float_as_uint(x) & 0xFFFFu) != 0u) continue;  // not a BF16 value
+      const float2 q = make_float2(x * r, x * r);
+      ok &= (cvt_e2m1x8(q, q, q, q) & 0xFu) == want[i];
+    }
+    if (ok) {
+      R = r;
+      return true;
+    }
+  }
+  return false;
+}
+
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -783,7 +839,7 @@ __device__ __forceinline__ float4 lds_f4(uint32_t a) {
 // The upper-bound quotient is within 2^-19.5 of the exact one, inside the 2^-15
 // decision tolerance's margin (the lower bound's 2^-19.9 gives 2^-16.4 of it).
 // The per-code reciprocals come from the shared table `tab` (scale_entry).
-template <int TDIR>
+template <int TDIR, bool TIE = false>
 __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const TensorConsts& tc,
                                         uint32_t tab, BlockOut& out) {
   const uint32_t bb = __float_as_uint(bmax);
@@ -791,8 +847,18 @@ __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const 
   const float2 b2 = make_float2(bmax, bmax);
   const float2 th = __fmul2_rn(b2, make_float2(tc.r6_hi, tc.r4_hi));
   const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
-  const uint32_t ph = cvt_e4m3x2(th.y, th.x), pl = cvt_e4m3x2(tl.y, tl.x);
-  ok &= (ph == pl);
+  const uint32_t ph = cvt_e4m3x2(th.y, th.x);
+  uint32_t pl = cvt_e4m3x2(tl.y, tl.x);
+  if (TIE && __builtin_expect(ph != pl, 0)) {
+    // bmax/(alpha*m) within 2^-17 of an E4M3 tie for a candidate: settle the
+    // scale code exactly in place (block_scale_code's test) instead of
+    // deferring the block -- frequent when alpha has few significant bits
+    const uint32_t lo6 = pl & 0xFFu, lo4 = (pl >> 8) & 0xFFu;
+    const uint32_t s6 = lo6 != (ph & 0xFFu) ? scale_tie(lo6, bmax, tc.alpha, 6.f) : lo6;
+    const uint32_t s4 = lo4 != ((ph >> 8) & 0xFFu) ? scale_tie(lo4, bmax, tc.alpha, 4.f) : lo4;
+    pl = s6 | (s4 << 8);
+  }
+  if (!TIE) ok &= (ph == pl);
 #if F46_TAB
   const float4 e6 = lds_f4(tab + ((pl << 4) & 0xFF0u));
   const float4 e4 = lds_f4(tab + ((pl >> 4) & 0xFF0u));
@@ -810,6 +876,7 @@ __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const 
   const float4 e6 = make_float4(rq2.x, rh2.x, DD.x, __uint_as_float(pl & 0xFFu));
   const float4 e4 = make_float4(rq2.y, rh2.y, DD.y, __uint_as_float(pl >> 8));
 #endif
+  // TDIR 3: the table's x field holds safe_recip's R (codes exact as computed)
   const float2 rq = TDIR == 1 ? make_float2(e6.y, e4.y) : make_float2(e6.x, e4.x);
   uint32_t a0, a1, b0, b1;  // M=6 and M=4 code words
   const float2 sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));

@@ -217,6 +217,9 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_FULL
 #define F46_FULL 1
 #endif
+#ifndef F46_T3
+#define F46_T3 1
+#endif
 #ifndef F46_STEP2
 #define F46_STEP2 0
 #endif
@@ -450,7 +453,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         // rewritten by the resolve pass (ordered after this by __syncwarp)
         bool ok;
         if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
-          ok = block46<TDIR>(x, bmax, tc, tab, o);
+          ok = block46<TDIR, true>(x, bmax, tc, tab, o);
         else
           ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
         *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
@@ -522,7 +525,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 // per-tile bookkeeping is warp-uniform (the warp index comes through a shuffle,
 // so the compiler keeps it in uniform registers and the bulk copy needs no
 // per-lane election loop).
-template <int DT, int MODE, int TDIR>
+template <int DT, int MODE, int TDIR, bool TIE = false>
 __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                             uint64_t* wb, uint32_t* dl, uint32_t t_begin,
                                             uint32_t t_end, uint32_t n_seg, uint32_t tab) {
@@ -572,7 +575,7 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
       BlockOut o;
       bool ok;
       if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
-        ok = block46<TDIR>(x, bmax, tc, tab, o);
+        ok = block46<TDIR, TIE>(x, bmax, tc, tab, o);
       else
         ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
       *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
@@ -650,6 +653,17 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   __shared__ __align__(16) float4 sctab[128];
   static_assert(kWarps * 32 >= 128, "one thread per scale code");
   if (threadIdx.x < 128) sctab[threadIdx.x] = scale_entry(threadIdx.x, tc.alpha);
+  // TDIR 0, adaptive, BF16: per-code exact-tie reciprocals (safe_recip); if
+  // every code has one the streaming loop runs as TDIR 3 (no upper-bound pass)
+  float rsafe = 0.f;
+  bool unsafe = false;
+  // (codes 1..126: 0 underflows and 0x7F is NaN, neither is ever a stored scale)
+  if (DT == DT_BF16 && MODE == ADAPTIVE && tc.tdir == 0 && !tc.force_exact && threadIdx.x < 127 &&
+      threadIdx.x > 0)
+    unsafe = !safe_recip(threadIdx.x, tc.alpha, rsafe);
+  const bool t3 = DT == DT_BF16 && MODE == ADAPTIVE && tc.tdir == 0 && !tc.force_exact &&
+                  !__syncthreads_or(unsafe) && F46_T3;
+  if (t3 && threadIdx.x < 127 && threadIdx.x > 0) sctab[threadIdx.x].x = rsafe;
   __syncthreads();
   const uint32_t tab = smem_u32(sctab);
   const uint32_t wsm = smem_u32(smem) + warp * (kStages * kTileBytes);
@@ -673,12 +687,23 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
       exact_block_global<DT>(ea, alpha_d, b, kb4, p.d_flags);
   } else if (full && F46_FULL) {
     if constexpr (DT == DT_BF16) {
-      switch (tc.tdir) {
+      switch (t3 ? 3 : tc.tdir) {
         case -1:
           stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
-          stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          if (MODE == ADAPTIVE && e4m3_ties_possible(tc.alpha))
+            stream_full<DT, MODE, 0, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          else
+            stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          break;
+        case 3:
+          if constexpr (MODE == ADAPTIVE) {
+            if (e4m3_ties_possible(tc.alpha))
+              stream_full<DT, MODE, 3, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            else
+              stream_full<DT, MODE, 3>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          }
           break;
         case 1:
           stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
@@ -690,12 +715,15 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
       stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if constexpr (DT == DT_BF16) {
-    switch (tc.tdir) {
+    switch (t3 ? 3 : tc.tdir) {
       case -1:
         seg_stream<DT, MODE, EXTRA, -1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 0:
         seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+        break;
+      case 3:
+        if constexpr (MODE == ADAPTIVE) seg_stream<DT, MODE, EXTRA, 3>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 1:
         seg_stream<DT, MODE, EXTRA, 1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);

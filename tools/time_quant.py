@@ -13,6 +13,9 @@ L = _lib.load()
 dev = torch.device("cuda")
 g = torch.Generator(device=dev).manual_seed(int(os.environ.get("SEED", 1234)))
 x = torch.randn(rows, cols, generator=g, device=dev) * float(os.environ.get("STD", 1.0))
+if os.environ.get("AMAX"):  # pin the tensor's amax (its tie direction): values scaled below it
+    x = x * (float(os.environ["AMAX"]) / (x.abs().max() * 1.001))
+    x.view(-1)[12345] = float(os.environ["AMAX"])
 x = x.to(torch.bfloat16) if dt == "bf16" else x
 DT = _lib.DT_BF16 if dt == "bf16" else _lib.DT_F32
 codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=dev)
@@ -53,7 +56,7 @@ ma = sum(ta) / len(ta)
 am = float(amax.item())
 al = float(torch.tensor(am, dtype=torch.float32) / torch.tensor(mcap, dtype=torch.float32))
 tdir = "-1" if al * mcap > am else ("+1" if al * mcap < am else "0")
-print(f"seed {os.environ.get('SEED', 1234)} tdir {tdir} ", end="")
+print(f"seed {os.environ.get('SEED', 1234)} amax {am} alpha {al} tdir {tdir} ", end="")
 print(f"{os.path.basename(os.environ.get('F46_LIB_PATH', 'default'))} {mode} {dt}: K2 {ms*1e3:.1f} us  {rows*cols*bpe/ms/1e6:.0f} GB/s | K1 amax {ma*1e3:.1f} us {rows*cols*(bpe-0.5625)/ma/1e6:.0f} GB/s")
 if os.environ.get("NODQ"):
     sys.exit(0)
