@@ -336,7 +336,7 @@ def timed_flushed(fn, flush, stream, n, warm=1):
     ts = []
     for i in range(n):
         flush(i)
-        torch.cuda._sleep(200_000)
+        torch.cuda._sleep(2_000_000)  # ~1 ms: covers the host enqueue of Python-level calls
         s, e = _events(2)
         s.record(stream)
         fn()
@@ -456,7 +456,7 @@ def run_b200(args):
     barrier()
     for i in range(args.steps):
         flush_buf(i)  # evict L2 (clean) outside the timed span
-        torch.cuda._sleep(200_000)  # device busy while the host enqueues the step
+        torch.cuda._sleep(2_000_000)  # ~1 ms: device busy while the host enqueues the step
         starts[i].record(stream)
         step(i)
         ends[i].record(stream)

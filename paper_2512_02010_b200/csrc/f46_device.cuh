@@ -876,7 +876,9 @@ __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const 
   const float4 e6 = make_float4(rq2.x, rh2.x, DD.x, __uint_as_float(pl & 0xFFu));
   const float4 e4 = make_float4(rq2.y, rh2.y, DD.y, __uint_as_float(pl >> 8));
 #endif
-  // TDIR 3: the table's x field holds safe_recip's R (codes exact as computed)
+  // TDIR 3: the table's x field holds safe_recip's R (codes exact as computed);
+  // TDIR 4: x holds whichever reciprocal gives exact codes for the tensor (the
+  // lower bound for -1, the upper bound for +1, safe_recip's R for 3)
   const float2 rq = TDIR == 1 ? make_float2(e6.y, e4.y) : make_float2(e6.x, e4.x);
   uint32_t a0, a1, b0, b1;  // M=6 and M=4 code words
   const float2 sq = make_float2(cand_codes(x, rq.x, tc.zero, a0, a1), cand_codes(x, rq.y, tc.zero, b0, b1));

@@ -42,6 +42,7 @@ namespace {
 constexpr int kStages = F46_STAGES;
 
 int num_sms() { return f46rt::num_sms(); }
+void udiv_magic(uint32_t d, uint32_t* magic, uint32_t* sh1, uint32_t* sh2);
 
 // ---------------------------------------------------------------------------
 // mbarrier / TMA helpers
@@ -94,6 +95,9 @@ struct QParams {
   // grouped launches (gridDim.y groups): per-group strides of x (bytes), codes
   // and scales_tc (bytes); d_amax / d_alpha_out are indexed by the group
   int64_t g_x, g_codes, g_scales;
+  // flat streaming: block b -> row b / nb as t = umulhi(b, nb_magic),
+  // row = (t + ((b - t) >> nb_sh1)) >> nb_sh2 (udiv_magic, set by the launcher)
+  uint32_t nb_magic, nb_sh1, nb_sh2;
 };
 
 // Point the parameters at group blockIdx.y of a grouped launch.
@@ -216,6 +220,12 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #endif
 #ifndef F46_FULL
 #define F46_FULL 1
+#endif
+#ifndef F46_FLAT
+#define F46_FLAT 1
+#endif
+#ifndef F46_T4
+#define F46_T4 1
 #endif
 #ifndef F46_T3
 #define F46_T3 1
@@ -376,7 +386,7 @@ constexpr int kBPL = kSegElems / 512;   // blocks per lane per segment
 constexpr int kDefer = 2 * kSegElems / 16;  // deferred-block slots per warp (a segment defers <= half)
 
 // The streaming loop of one warp, specialised on the tensor-wide tie direction.
-template <int DT, int MODE, bool EXTRA, int TDIR>
+template <int DT, int MODE, bool EXTRA, int TDIR, bool TIE = false>
 __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                            uint64_t* wb, uint32_t* dl, uint32_t t_begin,
                                            uint32_t t_end, uint32_t tab) {
@@ -453,7 +463,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
         // rewritten by the resolve pass (ordered after this by __syncwarp)
         bool ok;
         if constexpr (F46_V3 && MODE == ADAPTIVE && TDIR != 2)
-          ok = block46<TDIR, true>(x, bmax, tc, tab, o);
+          ok = block46<TDIR, TIE>(x, bmax, tc, tab, o);
         else
           ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
         *reinterpret_cast<uint64_t*>(p.codes + coff + j * 256) = o.codes;
@@ -525,7 +535,12 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 // per-tile bookkeeping is warp-uniform (the warp index comes through a shuffle,
 // so the compiler keeps it in uniform registers and the bulk copy needs no
 // per-lane election loop).
-template <int DT, int MODE, int TDIR, bool TIE = false>
+//
+// FLAT (any cols % 16 == 0): the blocks of the tensor are one contiguous
+// sequence (blocks never straddle rows), so tile t is blocks [128t, 128t+128)
+// of it whatever the row length -- no partial per-row segments -- and each
+// block's (row, kb) for the scale layout comes from a multiply-high division.
+template <int DT, int MODE, int TDIR, bool TIE = false, bool FLAT = false>
 __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                             uint64_t* wb, uint32_t* dl, uint32_t t_begin,
                                             uint32_t t_end, uint32_t n_seg, uint32_t tab) {
@@ -536,15 +551,21 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
   const uint32_t nb = (uint32_t)p.cols >> 4;
   const uint32_t kb4 = (nb + 3) >> 2;
   const uint8_t* xb = reinterpret_cast<const uint8_t*>(p.x);
+  const uint32_t nblk = (uint32_t)p.rows * nb;
+  auto tile_bytes = [&](uint32_t tt) -> uint32_t {  // the last flat tile may be short
+    if constexpr (FLAT) return min(kSegBlocks, nblk - tt * kSegBlocks) * (16 * kEsz);
+    return kTileBytes;
+  };
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s)
       if (t_begin + s < t_end) {
-        mbar_expect_tx(&wb[s], kTileBytes);
-        bulk_load(wsm + s * kTileBytes, xb + (size_t)(t_begin + s) * kTileBytes, kTileBytes, &wb[s]);
+        const uint32_t nbytes = tile_bytes(t_begin + s);
+        mbar_expect_tx(&wb[s], nbytes);
+        bulk_load(wsm + s * kTileBytes, xb + (size_t)(t_begin + s) * kTileBytes, nbytes, &wb[s]);
       }
   }
-  uint32_t row = t_begin / n_seg, seg = t_begin - row * n_seg;
+  uint32_t row = FLAT ? 0 : t_begin / n_seg, seg = FLAT ? 0 : t_begin - row * n_seg;
   auto sf_row = [&](uint32_t r) -> uint32_t {  // lane's scale byte for block 0 of row r
     return ((r >> 7) * kb4 + (lane >> 2)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (lane & 3);
   };
@@ -578,9 +599,21 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
         ok = block46<TDIR, TIE>(x, bmax, tc, tab, o);
       else
         ok = block_sl<MODE, TDIR>(x, bmax, tc, SegLoad<DT>{blk_addr}, o);
-      *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
-      p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
-      fails |= (ok ? 0u : 1u) << j;
+      if constexpr (FLAT) {
+        const uint32_t b = t * kSegBlocks + lane + 32 * j;
+        const uint32_t hi = __umulhi(b, p.nb_magic);
+        const uint32_t r = (hi + ((b - hi) >> p.nb_sh1)) >> p.nb_sh2, kb = b - r * nb;
+        if (b < nblk) {
+          *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
+          p.scales_tc[((r >> 7) * kb4 + (kb >> 2)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (kb & 3)] =
+              (uint8_t)o.sc;
+          fails |= (ok ? 0u : 1u) << j;
+        }
+      } else {
+        *reinterpret_cast<uint64_t*>(cptr + j * 256) = o.codes;
+        p.scales_tc[soff + j * 4096] = (uint8_t)o.sc;
+        fails |= (ok ? 0u : 1u) << j;
+      }
     }
     if (__builtin_expect(__any_sync(0xFFFFFFFFu, fails != 0), 0)) {
       const uint32_t rbk = t * kSegBlocks;
@@ -600,12 +633,13 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
     }
     __syncwarp();
     if (lane == 0 && t + kStages < t_end) {
-      mbar_expect_tx(&wb[S], kTileBytes);
-      bulk_load(wsm + S * kTileBytes, xb + (size_t)(t + kStages) * kTileBytes, kTileBytes, &wb[S]);
+      const uint32_t nbytes = tile_bytes(t + kStages);
+      mbar_expect_tx(&wb[S], nbytes);
+      bulk_load(wsm + S * kTileBytes, xb + (size_t)(t + kStages) * kTileBytes, nbytes, &wb[S]);
     }
     ++t;
     cptr += kSegBlocks * 8;
-    if (++seg == n_seg) {
+    if (!FLAT && ++seg == n_seg) {
       seg = 0;
       ++row;
       srow = sf_row(row);
@@ -639,7 +673,9 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   const uint32_t kb4 = (nb + 3) >> 2;
   const uint32_t n_seg = (cols + kSegElems - 1) / kSegElems;
   const bool full = !EXTRA && (cols % kSegElems) == 0;
-  const uint32_t total = (uint32_t)p.rows * n_seg;
+  const bool flat = !EXTRA && !full && F46_FLAT;
+  const uint32_t total = flat ? ((uint32_t)p.rows * nb + kSegElems / 16 - 1) / (kSegElems / 16)
+                              : (uint32_t)p.rows * n_seg;
   const uint32_t gw = blockIdx.x * kWarps + warp, G = gridDim.x * kWarps;
 
   const double alpha_d = resolve_alpha(p);
@@ -664,7 +700,15 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   const bool t3 = DT == DT_BF16 && MODE == ADAPTIVE && tc.tdir == 0 && !tc.force_exact &&
                   !__syncthreads_or(unsafe) && F46_T3;
   if (t3 && threadIdx.x < 127 && threadIdx.x > 0) sctab[threadIdx.x].x = rsafe;
+  // TDIR +1: the exact-code reciprocal is the upper bound (rh).  With this the
+  // table's x field is, for TDIR -1, +1 and 3 alike, the reciprocal whose codes
+  // are the reference's, and all three run one instantiation (TDIR 4): the
+  // tensors of one grouped launch share a single hot loop (instruction cache)
+  if (DT == DT_BF16 && MODE == ADAPTIVE && tc.tdir == 1 && threadIdx.x < 128)
+    sctab[threadIdx.x].x = sctab[threadIdx.x].y;
   __syncthreads();
+  const bool t4 = DT == DT_BF16 && MODE == ADAPTIVE && !tc.force_exact && F46_T4 &&
+                  (t3 || tc.tdir == -1 || tc.tdir == 1);
   const uint32_t tab = smem_u32(sctab);
   const uint32_t wsm = smem_u32(smem) + warp * (kStages * kTileBytes);
   uint64_t* wb = bars[warp];
@@ -685,9 +729,55 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
     const uint32_t nblk = (uint32_t)p.rows * nb;
     for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk; b += gridDim.x * blockDim.x)
       exact_block_global<DT>(ea, alpha_d, b, kb4, p.d_flags);
+  } else if (flat) {
+    if constexpr (DT == DT_BF16) {
+      const bool tie = MODE == ADAPTIVE && e4m3_ties_possible(tc.alpha);
+      switch (t4 ? 4 : (t3 ? 3 : tc.tdir)) {
+        case 4:
+          if constexpr (MODE == ADAPTIVE) {
+            if (tie)
+              stream_full<DT, MODE, 4, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            else
+              stream_full<DT, MODE, 4, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          }
+          break;
+        case -1:
+          stream_full<DT, MODE, -1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          break;
+        case 0:
+          if (tie)
+            stream_full<DT, MODE, 0, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          else
+            stream_full<DT, MODE, 0, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          break;
+        case 3:
+          if constexpr (MODE == ADAPTIVE) {
+            if (tie)
+              stream_full<DT, MODE, 3, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            else
+              stream_full<DT, MODE, 3, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          }
+          break;
+        case 1:
+          stream_full<DT, MODE, 1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          break;
+        default:
+          stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+      }
+    } else {
+      stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+    }
   } else if (full && F46_FULL) {
     if constexpr (DT == DT_BF16) {
-      switch (t3 ? 3 : tc.tdir) {
+      switch (t4 ? 4 : (t3 ? 3 : tc.tdir)) {
+        case 4:
+          if constexpr (MODE == ADAPTIVE) {
+            if (e4m3_ties_possible(tc.alpha))
+              stream_full<DT, MODE, 4, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            else
+              stream_full<DT, MODE, 4>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          }
+          break;
         case -1:
           stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
@@ -720,10 +810,18 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
         seg_stream<DT, MODE, EXTRA, -1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 0:
-        seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+        if (MODE == ADAPTIVE && e4m3_ties_possible(tc.alpha))
+          seg_stream<DT, MODE, EXTRA, 0, true>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+        else
+          seg_stream<DT, MODE, EXTRA, 0>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
         break;
       case 3:
-        if constexpr (MODE == ADAPTIVE) seg_stream<DT, MODE, EXTRA, 3>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+        if constexpr (MODE == ADAPTIVE) {
+          if (e4m3_ties_possible(tc.alpha))
+            seg_stream<DT, MODE, EXTRA, 3, true>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+          else
+            seg_stream<DT, MODE, EXTRA, 3>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+        }
         break;
       case 1:
         seg_stream<DT, MODE, EXTRA, 1>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
@@ -2760,6 +2858,8 @@ int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
   const int smem = kWarps * kStages * kTileBytes;
   const int ctas_per_sm =
       f46rt::configure((const void*)quant_seg_kernel<DT, MODE, EXTRA>, smem, kWarps * 32);
+  QParams pm = p;
+  udiv_magic((uint32_t)std::max<int64_t>(1, p.cols >> 4), &pm.nb_magic, &pm.nb_sh1, &pm.nb_sh2);
   // The kernel keeps 32-bit byte offsets: launch at most 2^31 input bytes at a
   // time, in whole 128-row slabs so each launch owns complete scale atoms.
   constexpr int64_t kEsz = (DT == DT_BF16) ? 2 : 4;
@@ -2775,11 +2875,11 @@ int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
     int64_t grid = ((int64_t)num_sms() * ctas_per_sm + groups - 1) / groups;
     grid = std::min(grid, (tiles + kWarps - 1) / kWarps);
     if (grid < 1) grid = 1;
-    quant_seg_kernel<DT, MODE, EXTRA><<<dim3((unsigned)grid, (unsigned)groups), kWarps * 32, smem, s>>>(p);
+    quant_seg_kernel<DT, MODE, EXTRA><<<dim3((unsigned)grid, (unsigned)groups), kWarps * 32, smem, s>>>(pm);
     return launch_status();
   }
   for (int64_t r0 = 0; r0 < p.rows; r0 += rows_max) {
-    QParams q = p;
+    QParams q = pm;
     q.rows = std::min(rows_max, p.rows - r0);
     q.x = reinterpret_cast<const uint8_t*>(p.x) + r0 * p.cols * kEsz;
     q.codes = p.codes + r0 * nb * 8;

@@ -245,3 +245,23 @@ def test_timed_instantiation_every_tie_direction(mode, amax):
 
 def test_tie_amax_cover_every_direction():
     assert {tie_direction(a, 1536.0) for a in TIE_AMAX} == {-1, 0, 1}
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6"])
+@pytest.mark.parametrize("shape", [(300, 2688), (129, 48), (5, 16), (1000, 4160), (3, 1856), (257, 272)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_timed_instantiation_flat_tiles(mode, shape, dtype):
+    """Row lengths that are not a multiple of the 2048-element tile take the
+    flat streaming loop (tiles of 128 consecutive blocks across rows, a short
+    last tile): codes and tcgen05 scales against the oracle."""
+    g = torch.Generator().manual_seed(shape[0] + shape[1])
+    x = (torch.randn(*shape, generator=g) * 1.7).to(dtype)
+    cfg = f46.QuantConfig(scale_mode=mode)
+    q = (f46.quantize_tensor_adaptive(x.cuda(), cfg) if mode == "adaptive"
+         else f46.quantize_tensor(x.cuda(), cfg))
+    ref = O.quantize(bits(x) if dtype == torch.bfloat16 else x.numpy(), mode)
+    assert q.alpha == ref["alpha"]
+    assert np.array_equal(q.packed_codes.cpu().numpy(), ref["codes"])
+    nb = -(-shape[1] // 16)
+    sc = f46.blockquant.tc_to_rowmajor(q.scales_tc, shape[0], nb).cpu().numpy()
+    assert np.array_equal(sc, ref["scales"].reshape(shape[0], -1))
