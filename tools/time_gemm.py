@@ -21,3 +21,15 @@ for _ in range(10):
     ts.append(a.elapsed_time(b))
 ms = sorted(ts)[len(ts) // 2]
 print(f"gemm {M}x{N}x{K} {od}: {ms*1e3:.1f} us  {2*M*N*K/ms/1e9:.1f} TFLOP/s")
+# back to back (as the vendor comparison tools/time_torch_fp4.py times it)
+reps = 10
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize()
+torch.cuda._sleep(1_000_000)
+a.record()
+for _ in range(reps):
+    f46.gemm_nvfp4(aq, bq, od, out=out)
+b.record()
+torch.cuda.synchronize()
+ms = a.elapsed_time(b) / reps
+print(f"gemm {M}x{N}x{K} {od} back-to-back: {ms*1e3:.1f} us  {2*M*N*K/ms/1e9:.1f} TFLOP/s")
