@@ -191,11 +191,14 @@ __global__ void __launch_bounds__(256, 2) rht_t_amax_kernel(RtParams p) {
   for (int64_t u = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); u < units; u += (int64_t)gridDim.x * 8) {
     const int64_t hu = u % nH, ku = u / nH;
     const int64_t h0 = hu * kUnitH + 2 * lane;
+    Col2<DT> cn;  // next token block's rows, in flight during this one
+    if (ku * kUnitK < nbT) load_pair<DT>(p, ku * kUnitK, h0, cn);
+#pragma unroll 1
     for (int kk = 0; kk < kUnitK; ++kk) {
       const int64_t k = ku * kUnitK + kk;
       if (k >= nbT) break;
-      Col2<DT> c;
-      load_pair<DT>(p, k, h0, c);
+      const Col2<DT> c = cn;
+      if (kk + 1 < kUnitK && k + 1 < nbT) load_pair<DT>(p, k + 1, h0, cn);
       bool ok[2] = {false, false};
       if constexpr (DT == DT_BF16) {
         float2 a[16];
