@@ -1304,7 +1304,7 @@ __device__ __noinline__ void quant2d_tile_exact(const Q2Params p, double alpha, 
 }
 
 #ifndef F46_Q2V2_MINB
-#define F46_Q2V2_MINB 4
+#define F46_Q2V2_MINB 3
 #endif
 constexpr int kQ2Row = 24;  // staged tile row stride (bf16): 48 bytes, 16-byte aligned
 
@@ -1398,12 +1398,55 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
     };
     uint64_t cw[2] = {0, 0};
     double err[2] = {0.0, 0.0};
+    // Adaptive MSE, fast tiles: certified f32 quotient-space errors (K2's
+    // scheme over 256 values).  With the tile's exact codes v and q = x*rq
+    // within 2^-19.9 of x/D, |S(f32) - S(exact)| <= 2^-14.4 tmax sqrt(S6+S4)
+    // (Cauchy-Schwarz over 256 terms, |q| <= 6.5) + 2^-20 (S6+S4) (f32 sums,
+    // D^2) + 2^-31.8 tmax^2 (second order); outside the (wider) tolerance the
+    // f32 comparison is the reference's, else the float64 sums below decide.
+    float s32[2] = {0.f, 0.f};
+    const bool f32dec = MSE && p.mode == ADAPTIVE;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       if (k >= ncand) break;
       const float delta = e4m3_to_f32(sc[k]);
-      const uint64_t codes =
-          exact_codes(x2, rcp_approx(tcs.alpha * delta) * F46_QLO, tcs.alpha, delta, tcs.tdir, gload);
+      const float rq = rcp_approx(tcs.alpha * delta) * F46_QLO;
+      const uint64_t codes = exact_codes(x2, rq, tcs.alpha, delta, tcs.tdir, gload);
+      cw[k] = codes;
+      if (f32dec) {
+        uint32_t v[8];
+        unpack_e2m1x8((uint32_t)codes ^ tcs.zero, *reinterpret_cast<uint32_t(*)[4]>(&v[0]));
+        unpack_e2m1x8((uint32_t)(codes >> 32) ^ tcs.zero, *reinterpret_cast<uint32_t(*)[4]>(&v[4]));
+        const float2 r2 = make_float2(rq, rq);
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int pp = 0; pp < 8; ++pp) {
+          const float2 qv = __fmul2_rn(x2[pp], r2);
+          const float2 r = make_float2(fhadd_h<0>(v[pp], -qv.x), fhadd_h<1>(v[pp], -qv.y));
+          acc = __ffma2_rn(r, r, acc);
+        }
+        float t = acc.x + acc.y;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) t += __shfl_down_sync(FULL, t, o);
+        const float D = tcs.alpha * delta;
+        s32[k] = __shfl_sync(FULL, t, hbase) * (D * D);
+      }
+    }
+    bool need64 = !f32dec;
+    if (f32dec) {
+      const float ssum = s32[0] + s32[1];
+      const float tol = fmaf(0x1.6a09e6p-14f * tmax, sqrt_approx(ssum),  // 2^-13.5
+                             fmaf(0x1p-18f, ssum, fmaf(0x1p-30f * tmax, tmax, 0x1p-140f)));
+      need64 = fast && !(fabsf(s32[0] - s32[1]) > tol);
+      err[0] = s32[0];
+      err[1] = s32[1];
+    }
+    if (__any_sync(FULL, need64)) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (k >= ncand) break;
+      const float delta = e4m3_to_f32(sc[k]);
+      const uint64_t codes = cw[k];
       const double denom = (double)tcs.alpha * (double)delta;  // exact
       double r = 0.0, mx = 0.0;
 #pragma unroll
@@ -1426,8 +1469,8 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
         const double t = __dadd_rn(c, __shfl_down_sync(FULL, c, 8));   // lane (0, 0)
         tot = __shfl_sync(FULL, t, hbase);
       }
-      cw[k] = codes;
-      err[k] = tot;
+      if (need64) err[k] = tot;
+    }
     }
     const bool k4 = (p.mode == ADAPTIVE) ? (err[1] < err[0]) : (p.mode == FIXED4);
     const int ki = (p.mode == ADAPTIVE && k4) ? 1 : 0;
