@@ -219,6 +219,20 @@ int f46_rht16(const void* x, int dtype, int64_t n, const double* signs16, double
               f46_stream_t stream);
 
 /*
+ * Fused amax + quantize in one cooperative launch for tensors that fit in L2
+ * (< 2^31 bytes; worthwhile up to ~96 MB): each warp takes max|x| over
+ * exactly the tiles it then quantizes, a grid-wide barrier publishes the
+ * tensor amax, and the quantize pass re-reads its tiles from L2.  Identical
+ * output to f46_amax + f46_quantize.  d_work: device 16 bytes, zeroed by the
+ * caller (the float64 amax, then the barrier counter); no alpha override and
+ * no parity views.  F46_ERR_UNSUPPORTED when the tensor or the device does
+ * not allow it (the caller then runs the two-kernel path).
+ */
+int f46_quantize_fused(const void* x, int dtype, int64_t rows, int64_t cols, int mode, int rule,
+                       double mcap, double* d_work, uint8_t* codes, uint8_t* scales_tc,
+                       double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream);
+
+/*
  * Grouped (expert-parallel MoE) variants.  A grouped
  * tensor is `groups` equal tensors stored back to back; each group is its own
  * reference tensor with its own tensor scale (d_amax[g], d_alpha_out[g]), i.e.

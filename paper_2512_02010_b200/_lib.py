@@ -53,6 +53,7 @@ EXPORTS = (
     "f46_quantize_block_ref",
     "f46_matmul_f32_ordered",
     "f46_set_test_hook",
+    "f46_quantize_fused",
     "f46_build_info",
 )
 
@@ -105,6 +106,8 @@ def _declare(L):
     L.f46_quantize_block_ref.restype = i
     L.f46_matmul_f32_ordered.argtypes = [p, p, i64, i64, i64, p, p]
     L.f46_matmul_f32_ordered.restype = i
+    L.f46_quantize_fused.argtypes = [p, i, i64, i64, i, i, d, p, p, p, p, p, p]
+    L.f46_quantize_fused.restype = i
     L.f46_set_test_hook.argtypes = [i, i64]
     L.f46_set_test_hook.restype = i
     L.f46_build_info.argtypes = []

@@ -352,6 +352,10 @@ def sr_keys(seed: int, sr_tag: int) -> tuple[int, int, int, int]:
     return int(k6[0]), int(k6[1]), int(k4[0]), int(k4[1])
 
 
+# tensors up to this size take the fused single-launch amax + quantize
+FUSED_MAX_BYTES = int(__import__('os').environ.get('F46_FUSED_MAX_MB', '96')) << 20
+
+
 def quantize_1d(X, mode: str, rule: str = "mse", fp8_cap: float = 448.0, alpha=None, *,
                 d_amax: Optional[torch.Tensor] = None, check_finite: bool = True,
                 want_rowmajor: bool = False, want_pick4: bool = False,
@@ -380,6 +384,23 @@ def quantize_1d(X, mode: str, rule: str = "mse", fp8_cap: float = 448.0, alpha=N
     a_over = 0.0
     if alpha is not None:
         a_over = _check_alpha_override(alpha)
+    elif (d_amax is None and rounding == "rne" and scales_rm is None and pick4 is None
+          and t.dtype != torch.float64 and t.numel() * t.element_size() <= FUSED_MAX_BYTES):
+        # L2-sized tensor: amax and quantize in one cooperative launch (the
+        # quantize pass re-reads its tiles from L2)
+        work = torch.zeros(2, dtype=torch.float64, device=dev)
+        rc = L.f46_quantize_fused(t.data_ptr(), _DT_OF[t.dtype], rows, cols, _lib.MODE[mode],
+                                  _lib.RULE[rule], mcap, work.data_ptr(), codes.data_ptr(),
+                                  scales_tc.data_ptr(), alpha_dev.data_ptr(), flags.data_ptr(),
+                                  _stream())
+        if rc == _lib.F46_OK:
+            if check_finite:
+                _raise_flags(flags)
+            shape = tuple(X.shape) if hasattr(X, "shape") else tuple(t.shape)
+            return QuantizedTensor._from_device(shape, "nvfp4", codes, scales_tc, alpha_dev)
+        if rc != _lib.F46_ERR_UNSUPPORTED:
+            _lib.check(rc, "f46_quantize_fused")
+        d_amax = amax_device(t)
     elif d_amax is None:
         d_amax = amax_device(t)
     if rounding == "sr":

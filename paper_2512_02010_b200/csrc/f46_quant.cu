@@ -98,6 +98,9 @@ struct QParams {
   // flat streaming: block b -> row b / nb as t = umulhi(b, nb_magic),
   // row = (t + ((b - t) >> nb_sh1)) >> nb_sh2 (udiv_magic, set by the launcher)
   uint32_t nb_magic, nb_sh1, nb_sh2;
+  // fused amax + quantize (f46_quantize_fused): grid-barrier counter, zeroed
+  // by the caller with d_amax; null for the two-kernel path
+  uint32_t* d_sync;
 };
 
 // Point the parameters at group blockIdx.y of a grouped launch.
@@ -116,7 +119,7 @@ __device__ __forceinline__ void select_group(QParams& p) {
 // for an all-zero tensor, or the override.
 __device__ __forceinline__ double resolve_alpha(const QParams& p) {
   if (p.alpha_override > 0.0) return p.alpha_override;
-  const double amax = *p.d_amax;
+  const double amax = __ldcg(p.d_amax);
   if (amax == 0.0) return 1.0;
   return (double)((float)amax / (float)p.mcap);
 }
@@ -125,7 +128,7 @@ __device__ __forceinline__ void prologue_flags(const QParams& p, double alpha) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (p.d_alpha_out) *p.d_alpha_out = alpha;
     if (p.alpha_override <= 0.0 && p.d_flags) {
-      const double amax = *p.d_amax;
+      const double amax = __ldcg(p.d_amax);
       if (!(amax <= 1.7976931348623157e308)) atomicOr(p.d_flags, F46_FLAG_NONFINITE);
     }
   }
@@ -224,6 +227,10 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_FLAT
 #define F46_FLAT 1
 #endif
+#ifndef F46_SF_UNROLL
+#define F46_SF_UNROLL 4
+#endif
+constexpr int kSfUnroll = F46_SF_UNROLL;
 #ifndef F46_T4
 #define F46_T4 1
 #endif
@@ -587,7 +594,7 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
     const uint32_t blk0 = wsm + S * kTileBytes + lane * (16 * kEsz);
     const uint32_t soff = srow + seg * (kSegBlocks / 4) * 512;
     uint32_t fails = 0;
-#pragma unroll
+#pragma unroll kSfUnroll
     for (int j = 0; j < kBPL; ++j) {
       const uint32_t blk_addr = blk0 + j * (32 * 16 * kEsz);
       float2 x[8];
@@ -678,12 +685,63 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
                               : (uint32_t)p.rows * n_seg;
   const uint32_t gw = blockIdx.x * kWarps + warp, G = gridDim.x * kWarps;
 
+  if (!EXTRA && p.d_sync) {
+    // fused K1: max|x| over exactly the tiles this warp quantizes below (so
+    // they are in L2 for the second pass), one 64-bit atomicMax per warp on the
+    // float64 bit pattern as amax_kernel, then a grid-wide barrier (the launch
+    // is cooperative: every CTA is resident)
+    const uint32_t per0 = total / G, rem0 = total - per0 * G;
+    const uint32_t tb = gw * per0 + min(gw, rem0), te = tb + per0 + (gw < rem0 ? 1u : 0u);
+    const uint64_t nbytes = (uint64_t)p.rows * p.cols * kEsz;
+    const uint64_t b0 = (uint64_t)tb * kTileBytes, b1 = min((uint64_t)te * kTileBytes, nbytes);
+    const uint4* xv = reinterpret_cast<const uint4*>(p.x);
+    uint32_t m = 0;
+    auto fold = [&](const uint4 v) {
+      if constexpr (DT == DT_BF16) {
+        m = __vmaxu2(m, v.x & 0x7FFF7FFFu);
+        m = __vmaxu2(m, v.y & 0x7FFF7FFFu);
+        m = __vmaxu2(m, v.z & 0x7FFF7FFFu);
+        m = __vmaxu2(m, v.w & 0x7FFF7FFFu);
+      } else {
+        m = max(m, max(max(v.x & 0x7FFFFFFFu, v.y & 0x7FFFFFFFu), max(v.z & 0x7FFFFFFFu, v.w & 0x7FFFFFFFu)));
+      }
+    };
+    // eight 16-byte loads in flight per lane (4 KB per warp step)
+    uint64_t off = b0 + lane * 16;
+    for (; off + 7 * 512 < b1; off += 8 * 512) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = xv[(off + u * 512) >> 4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fold(v[u]);
+    }
+    for (; off < b1; off += 512) fold(xv[off >> 4]);
+    if constexpr (DT == DT_BF16) m = max(m & 0xFFFFu, m >> 16) << 16;
+    uint64_t m64 = (uint64_t)__double_as_longlong((double)__uint_as_float(m));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, m64, o);
+      m64 = v > m64 ? v : m64;
+    }
+    if (lane == 0 && m64) atomicMax(reinterpret_cast<unsigned long long*>(const_cast<double*>(p.d_amax)),
+                                    (unsigned long long)m64);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(p.d_sync, 1u);
+      const uint32_t want = gridDim.x * gridDim.y;
+      while (*reinterpret_cast<volatile uint32_t*>(p.d_sync) < want) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+  }
+
   const double alpha_d = resolve_alpha(p);
   prologue_flags(p, alpha_d);
   const bool overridden = p.alpha_override > 0.0;
   const TensorConsts tc = make_consts(
       alpha_d, p.rule, DT,
-      tie_direction(alpha_d, overridden ? 0.0 : *p.d_amax, p.mcap, DT, overridden));
+      tie_direction(alpha_d, overridden ? 0.0 : __ldcg(p.d_amax), p.mcap, DT, overridden));
 
   // per-tensor table of the per-scale-code reciprocals (block46)
   __shared__ __align__(16) float4 sctab[128];
@@ -3120,6 +3178,53 @@ int f46_quantize(const void* x, int dtype, int64_t rows, int64_t cols, int mode,
     default:
       return F46_ERR_INVALID_ARG;
   }
+}
+
+int f46_quantize_fused(const void* x, int dtype, int64_t rows, int64_t cols, int mode, int rule,
+                       double mcap, double* d_work, uint8_t* codes, uint8_t* scales_tc,
+                       double* d_alpha_out, uint32_t* d_flags, f46_stream_t stream) {
+  if (!x || !codes || !scales_tc || !d_work || rows <= 0 || cols <= 0 || !(mcap > 0.0))
+    return F46_ERR_INVALID_ARG;
+  if (mode < F46_FIXED6 || mode > F46_ADAPTIVE || rule < F46_RULE_MSE || rule > F46_RULE_ABSMAX)
+    return F46_ERR_CONFIG;
+  if (dtype != F46_DT_BF16 && dtype != F46_DT_F32) return F46_ERR_UNSUPPORTED;
+  const int64_t esz = dtype == F46_DT_BF16 ? 2 : 4;
+  if (cols % 16 || ((uintptr_t)x & 15) || ((uintptr_t)codes & 7) || rows * cols * esz >= (1ll << 31))
+    return F46_ERR_UNSUPPORTED;
+  QParams p{x, rows, cols, mode, rule, dtype, mcap, d_work, 0.0, codes, scales_tc, nullptr,
+            nullptr, d_alpha_out, d_flags};
+  udiv_magic((uint32_t)std::max<int64_t>(1, cols >> 4), &p.nb_magic, &p.nb_sh1, &p.nb_sh2);
+  p.d_sync = reinterpret_cast<uint32_t*>(d_work + 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto launch = [&](const void* kernel, int smem) -> int {
+    const int per_sm = f46rt::configure(kernel, smem, kWarps * 32);
+    const int64_t tiles = rows * ((cols + kSegElems - 1) / kSegElems);
+    int64_t grid = std::min<int64_t>((tiles + kWarps - 1) / kWarps, (int64_t)num_sms() * per_sm);
+    if (grid < 1) grid = 1;
+    void* args[] = {&p};
+    const cudaError_t e = cudaLaunchCooperativeKernel(kernel, dim3((unsigned)grid), dim3(kWarps * 32),
+                                                      args, (size_t)smem, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return F46_ERR_UNSUPPORTED;
+    }
+    return F46_OK;
+  };
+  const int smem_bf16 = kWarps * kStages * kSegElems * 2, smem_f32 = kWarps * kStages * kSegElems * 4;
+#define F46_FUSED(DTV, MV, SMEM) launch((const void*)quant_seg_kernel<DTV, MV, false>, SMEM)
+  if (dtype == F46_DT_BF16) {
+    switch (mode) {
+      case F46_FIXED6: return F46_FUSED(DT_BF16, FIXED6, smem_bf16);
+      case F46_FIXED4: return F46_FUSED(DT_BF16, FIXED4, smem_bf16);
+      default: return F46_FUSED(DT_BF16, ADAPTIVE, smem_bf16);
+    }
+  }
+  switch (mode) {
+    case F46_FIXED6: return F46_FUSED(DT_F32, FIXED6, smem_f32);
+    case F46_FIXED4: return F46_FUSED(DT_F32, FIXED4, smem_f32);
+    default: return F46_FUSED(DT_F32, ADAPTIVE, smem_f32);
+  }
+#undef F46_FUSED
 }
 
 int f46_amax_grouped(const void* x, int dtype, int groups, int64_t n, double* d_amax,

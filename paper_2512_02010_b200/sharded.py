@@ -113,12 +113,18 @@ class ShardedQuantizer:
         self.codes = torch.empty((self.rows, nb * 8), dtype=torch.uint8, device=device)
         self.scales_tc = torch.zeros(scales_tc_bytes(self.rows, self.cols), dtype=torch.uint8,
                                      device=device)
-        self.amax = torch.zeros(1, dtype=torch.float64, device=device)
+        # [amax (float64), barrier counter] for f46_quantize_fused; amax is its first word
+        self.work = torch.zeros(2, dtype=torch.float64, device=device)
+        self.amax = self.work[:1]
         self.alpha = torch.empty(1, dtype=torch.float64, device=device)
         self.flags = torch.zeros(1, dtype=torch.int32, device=device)
         self.all_reduce_max = all_reduce_max
         self._L = _lib.load()
         self._lib = _lib
+        from .blockquant import FUSED_MAX_BYTES
+
+        esz = torch.empty(0, dtype=dtype).element_size()
+        self.fused = self.rows * self.cols * esz <= FUSED_MAX_BYTES
 
     def amax_local(self, x, stream: int) -> None:
         """K1 over the local slab into self.amax (zeroed first)."""
@@ -145,6 +151,16 @@ class ShardedQuantizer:
         if tuple(x.shape) != (self.rows, self.cols) or not x.is_contiguous():
             raise ValueError(f"expected a contiguous ({self.rows}, {self.cols}) slab")
         s = torch.cuda.current_stream().cuda_stream if stream is None else stream
+        if self.all_reduce_max is None and self.fused:
+            # single rank, L2-sized slab: one cooperative launch (f46_quantize_fused)
+            self.work.zero_()
+            rc = self._L.f46_quantize_fused(
+                x.data_ptr(), self.dt, self.rows, self.cols, self._lib.MODE[self.mode], 0, self.mcap,
+                self.work.data_ptr(), self.codes.data_ptr(), self.scales_tc.data_ptr(),
+                self.alpha.data_ptr(), None, s)
+            if rc == self._lib.F46_OK:
+                return
+            self.fused = False
         self.amax_local(x, s)
         self.exchange()
         self.quantize_local(x, s)

@@ -265,3 +265,43 @@ def test_timed_instantiation_flat_tiles(mode, shape, dtype):
     nb = -(-shape[1] // 16)
     sc = f46.blockquant.tc_to_rowmajor(q.scales_tc, shape[0], nb).cpu().numpy()
     assert np.array_equal(sc, ref["scales"].reshape(shape[0], -1))
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (300, 2688), (17, 48), (1024, 14336)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("mode", ["adaptive", "fixed4"])
+def test_fused_single_launch_equals_two_kernels(shape, dtype, mode):
+    """f46_quantize_fused (amax and quantize in one cooperative launch, the
+    path quantize_tensor* takes for L2-sized tensors) == f46_amax +
+    f46_quantize, and both == the oracle."""
+    from paper_2512_02010_b200 import _lib
+    from paper_2512_02010_b200.blockquant import scales_tc_bytes
+    g = torch.Generator().manual_seed(shape[1])
+    x = (torch.randn(*shape, generator=g) * 0.7).to(dtype).cuda()
+    L = _lib.load()
+    rows, cols = shape
+    mcap = {"adaptive": 1536.0, "fixed4": 1792.0}[mode]
+    dt = _lib.DT_BF16 if dtype == torch.bfloat16 else _lib.DT_F32
+    outs = []
+    for fused in (True, False):
+        codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device="cuda")
+        sc = torch.zeros(scales_tc_bytes(rows, cols), dtype=torch.uint8, device="cuda")
+        alpha = torch.empty(1, dtype=torch.float64, device="cuda")
+        work = torch.zeros(2, dtype=torch.float64, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        if fused:
+            assert L.f46_quantize_fused(x.data_ptr(), dt, rows, cols, _lib.MODE[mode], 0, mcap,
+                                        work.data_ptr(), codes.data_ptr(), sc.data_ptr(),
+                                        alpha.data_ptr(), None, s) == 0
+        else:
+            assert L.f46_amax(x.data_ptr(), dt, x.numel(), work.data_ptr(), s) == 0
+            assert L.f46_quantize(x.data_ptr(), dt, rows, cols, _lib.MODE[mode], 0, mcap,
+                                  work.data_ptr(), 0.0, codes.data_ptr(), sc.data_ptr(), None, None,
+                                  alpha.data_ptr(), None, s) == 0
+        outs.append((codes, sc, alpha, work[0].clone()))
+    (c1, s1, a1, m1), (c2, s2, a2, m2) = outs
+    assert torch.equal(m1, m2) and torch.equal(a1, a2)
+    assert torch.equal(c1, c2) and torch.equal(s1, s2)
+    ref = O.quantize(bits(x.cpu()) if dtype == torch.bfloat16 else x.cpu().numpy(), mode)
+    assert float(a1.item()) == ref["alpha"]
+    assert np.array_equal(c1.cpu().numpy(), ref["codes"])
