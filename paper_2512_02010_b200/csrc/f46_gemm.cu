@@ -545,7 +545,10 @@ constexpr int smem_bytes_pair() {
   return PairCfg<OUT_BF16>::kStages * PSTAGE_BYTES + PairCfg<OUT_BF16>::kStaging + 1024 + 1024;
 }
 constexpr int kSfWarps = 4;
-constexpr int kSfBufs = 4;  // TMEM scale buffers: 256 + 4 x 48 = 448 columns
+#ifndef F46_SF_BUFS
+#define F46_SF_BUFS 4
+#endif
+constexpr int kSfBufs = F46_SF_BUFS;  // TMEM scale buffers: 256 + kSfBufs x 48 <= 512 columns
 constexpr int kThreadsPair = 64 + 32 * kEpiWarps + 32 * kSfWarps;
 constexpr uint32_t kIdescPair = (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                 ((uint32_t)(256 >> 4) << 24);

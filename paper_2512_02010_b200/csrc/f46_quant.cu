@@ -1398,7 +1398,8 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
        t0 += G) {
     const int64_t tile = t0 + hw;
     const bool live = tile < ntiles;
-    const int64_t tr = live ? tile / TC : 0, tc = live ? tile - tr * TC : 0;
+    // (tile counts fit 32 bits: a 32-bit division, not the 64-bit one)
+    const int64_t tr = live ? (int64_t)((uint32_t)tile / (uint32_t)TC) : 0, tc = live ? tile - tr * TC : 0;
     const int64_t r0 = tr * 16 + 8 * h, c0 = tc * 16;
     // the lane's 16 values in accumulation order: (row r0 + i/2, col (i%2)*8 + j)
     float x[16];
@@ -1567,9 +1568,15 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
         // W^T rows c0 + j (even elements) and c0 + 8 + j (odd elements), word h
 #pragma unroll
         for (int par = 0; par < 2; ++par) {
-          uint32_t wt = 0;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) wt |= (uint32_t)((codes >> (4 * (2 * i + par))) & 0xFull) << (4 * i);
+          // nibbles par, par+2, ..., par+14 of the 16 codes, packed: per 32-bit
+          // half keep one nibble of every byte, then squeeze the bytes together
+          auto squeeze = [](uint32_t w) -> uint32_t {
+            w &= 0x0F0F0F0Fu;
+            w = (w | (w >> 4)) & 0x00FF00FFu;
+            return (w | (w >> 8)) & 0x0000FFFFu;
+          };
+          const uint32_t lo = (uint32_t)codes >> (4 * par), hi = (uint32_t)(codes >> 32) >> (4 * par);
+          uint32_t wt = squeeze(lo) | (squeeze(hi) << 16);
           const int64_t rt = c0 + 8 * par + j;
           if (rt < p.C && r0 < p.R) {
             if (r0 + 8 > p.R) wt &= (1u << (4 * (int)(p.R - r0))) - 1u;  // pad rows of W
