@@ -289,7 +289,10 @@ constexpr int kStagesP = 4;
 constexpr int SMEM_BYTES_P = kStagesP * STAGE_BYTES + 1024 + 1024;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, 128 columns each
 constexpr int kThreadsP = 64 + 32 * kEpiWarps;
-constexpr int kGroupM = 16;  // raster band height (m-tiles) for L2 reuse
+#ifndef F46_GROUP_M
+#define F46_GROUP_M 16
+#endif
+constexpr int kGroupM = F46_GROUP_M;  // raster band height (m-tiles) for L2 reuse
 
 struct TileCoord {
   int g, mt, nt;
@@ -796,7 +799,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
 #endif
-#if F46_EPI_BATCH
+#if F46_EPI_BATCH == 2
+        // all four TMEM loads in flight, one wait, release, then convert
+        {
+          uint32_t ra[32], rb[32], rc[32], rd[32];
+          tc_ld_32x32b_x32(taddr, ra);
+          tc_ld_32x32b_x32(taddr + 32, rb);
+          tc_ld_32x32b_x32(taddr + 64, rc);
+          tc_ld_32x32b_x32(taddr + 96, rd);
+          tc_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(leader_acc_empty);
+          emit(ra, 0);
+          emit(rb, 1);
+          emit(rc, 2);
+          emit(rd, 3);
+        }
+#elif F46_EPI_BATCH
         // two TMEM loads per wait: the accumulator is drained in two round trips
         {
           uint32_t ra[32], rb[32];
