@@ -227,6 +227,18 @@ constexpr int kKbUnroll = F46_KB_UNROLL;
 #ifndef F46_FLAT
 #define F46_FLAT 1
 #endif
+#ifndef F46_PAR_RESOLVE
+#define F46_PAR_RESOLVE 1
+#endif
+// inputs up to this size take the parallel-resolver instantiation (the fused
+// amax+quantize path's range)
+constexpr int64_t kParResolveMaxBytes = (int64_t)96 << 20;
+#ifndef F46_RL_INLINE
+#define F46_RL_INLINE __noinline__
+#endif
+#ifndef F46_NO_DEFER_PROBE
+#define F46_NO_DEFER_PROBE 0
+#endif
 #ifndef F46_SF_UNROLL
 #define F46_SF_UNROLL 4
 #endif
@@ -389,6 +401,124 @@ __device__ __noinline__ void resolve_block_global(ExactArgs a, TensorConsts tc, 
   if (a.pick4) a.pick4[blk] = (uint8_t)o.pick4;
 }
 
+// Two deferred blocks per warp, 16 lanes each (lane i of a half owns element
+// i): the exact answer of resolve_block_global -- scale codes from the exact
+// tie test, codes from the proven bracket logic per element, the two squared
+// error sums in float64 in numpy's pairwise order (r_j = e_j + e_{j+8}, then
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), blockquant.py:289-290) through
+// half-warp shuffles, strict '<' (adaptive.py:77-80) -- with the element work
+// spread over the lanes, so the resolve pass after the hot loop is short.
+// Zero, tiny, huge, non-finite and underflowing blocks keep the single-lane
+// float64 restatement (exact_block_global).  All 32 lanes call it.
+__device__ __forceinline__ uint32_t exact_code_elem(float x, float rq, float alpha, float delta,
+                                                    int tdir) {
+  const float ql = x * rq, qh = ql * F46_QHI_OVER_QLO;
+  const uint32_t cl = cvt_e2m1x8(make_float2(ql, ql), make_float2(ql, ql), make_float2(ql, ql),
+                                 make_float2(ql, ql)) & 0xFu;
+  const uint32_t ch = cvt_e2m1x8(make_float2(qh, qh), make_float2(qh, qh), make_float2(qh, qh),
+                                 make_float2(qh, qh)) & 0xFu;
+  if (cl == ch) return cl;
+  if (tdir < 0) return cl;
+  if (tdir == 1) return ch;
+  if (tdir == 0) return (cl & 1u) ? ch : cl;  // an exact tie: the even code
+  const uint32_t m = cl & 7u;
+  const float s = fmaf(alpha, fp4_tie_above(m) * delta, -fabsf(x));
+  return cl + ((s < 0.f) | ((s == 0.f) & (m & 1u)));
+}
+
+template <int DT, int MODE>
+__device__ __forceinline__ void resolve_pair(const ExactArgs& a, const TensorConsts& tc, uint32_t kb4,
+                                             uint32_t* flags, uint32_t blk_lo, uint32_t blk_hi,
+                                             bool has_hi) {
+  const unsigned FULL = 0xFFFFFFFFu;
+  const int lane = threadIdx.x & 31, i = lane & 15;
+  const bool hi_half = lane >= 16;
+  const uint32_t blk = hi_half ? blk_hi : blk_lo;
+  const bool valid = !hi_half || has_hi;
+  const uint32_t nb = (uint32_t)(a.cols >> 4);
+  const uint32_t row = blk / nb, kbg = blk - row * nb;
+  const int64_t e0 = (int64_t)row * a.cols + (int64_t)kbg * 16;
+  float x = 0.f;
+  if (valid) {
+    if constexpr (DT == DT_BF16)
+      x = __uint_as_float((uint32_t)(reinterpret_cast<const uint16_t*>(a.x)[e0 + i]) << 16);
+    else
+      x = reinterpret_cast<const float*>(a.x)[e0 + i];
+  }
+  float bmax = fabsf(x);
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) bmax = fmax_nan(bmax, __shfl_xor_sync(FULL, bmax, o, 16));
+  const uint32_t bb = __float_as_uint(bmax);
+  const float alpha = tc.alpha;
+  uint32_t sc6 = 0, sc4 = 0;
+  bool special = (bb - 0x2B800000u) >= 0x28000000u;  // zero, tiny, huge or non-finite
+  if (!special) {
+    if constexpr (MODE == ADAPTIVE) {
+      sc6 = block_scale_code(bmax, alpha, 6.f, tc.r6_lo, tc.r6_hi);
+      sc4 = block_scale_code(bmax, alpha, 4.f, tc.r4_lo, tc.r4_hi);
+    } else {
+      sc6 = MODE == FIXED6 ? block_scale_code(bmax, alpha, 6.f, tc.r6_lo, tc.r6_hi)
+                           : block_scale_code(bmax, alpha, 4.f, tc.r4_lo, tc.r4_hi);
+      sc4 = sc6;
+    }
+    special = sc6 == 0 || sc4 == 0;
+  }
+  // every lane keeps shuffling (inactive and special halves with dummy values);
+  // special blocks are settled by one lane after the last shuffle
+  uint64_t word[2];
+  double S[2];
+  const int ncand = MODE == ADAPTIVE ? 2 : 1;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (k >= ncand) break;
+    const uint32_t sc = special ? 0x38u : (k == 0 ? sc6 : sc4);
+    const float delta = e4m3_to_f32(sc);
+    const float rq = rcp_approx(alpha * delta) * F46_QLO;
+    const uint32_t c = exact_code_elem(x, rq, alpha, delta, tc.tdir);
+    uint64_t w = (uint64_t)c << (4 * i);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) w |= __shfl_xor_sync(FULL, w, o, 16);
+    word[k] = w;
+    const double diff = __dsub_rn(__dmul_rn(dec_fp4_d(c), __dmul_rn(tc.alpha_d, (double)delta)),
+                                  (double)x);
+    const double e = __dmul_rn(diff, diff);
+    const double r = __dadd_rn(e, __shfl_down_sync(FULL, e, 8, 16));     // j < 8: e_j + e_{j+8}
+    const double p1 = __dadd_rn(r, __shfl_down_sync(FULL, r, 1, 16));    // j even
+    const double p2 = __dadd_rn(p1, __shfl_down_sync(FULL, p1, 2, 16));  // j % 4 == 0
+    const double p3 = __dadd_rn(p2, __shfl_down_sync(FULL, p2, 4, 16));  // j == 0
+    S[k] = __shfl_sync(FULL, p3, 0, 16);
+  }
+  if (!valid || i != 0) return;
+  if (special) {
+    exact_block_global<DT>(a, tc.alpha_d, blk, kb4, flags);
+    return;
+  }
+  BlockOut o;
+  if constexpr (MODE == ADAPTIVE) {
+    const bool k4 = S[1] < S[0];  // strict: ties keep 6
+    o.codes = k4 ? word[1] : word[0];
+    o.sc = k4 ? sc4 : sc6;
+    o.pick4 = k4;
+  } else {
+    o.codes = word[0];
+    o.sc = sc6;
+    o.pick4 = (MODE == FIXED4);
+  }
+  *reinterpret_cast<uint64_t*>(a.codes + (int64_t)blk * 8) = o.codes;
+  a.scales_tc[sf_tc_offset(row, kbg, kb4)] = (uint8_t)o.sc;
+  if (a.scales_rm) a.scales_rm[blk] = (uint8_t)o.sc;
+  if (a.pick4) a.pick4[blk] = (uint8_t)o.pick4;
+}
+
+// Resolve a warp's deferred-block list, two blocks per step (resolve_pair).
+template <int DT, int MODE>
+__device__ F46_RL_INLINE void resolve_list(const ExactArgs ea, const TensorConsts tc, uint32_t kb4,
+                                          uint32_t* flags, const uint32_t* dl, uint32_t n) {
+#pragma unroll 1
+  for (uint32_t i = 0; i < n; i += 2)
+    resolve_pair<DT, MODE>(ea, tc, kb4, flags, dl[i], dl[i + 1 < n ? i + 1 : i], i + 1 < n);
+}
+
 constexpr int kBPL = kSegElems / 512;   // blocks per lane per segment
 constexpr int kDefer = 2 * kSegElems / 16;  // deferred-block slots per warp (a segment defers <= half)
 
@@ -548,9 +678,9 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 // of it whatever the row length -- no partial per-row segments -- and each
 // block's (row, kb) for the scale layout comes from a multiply-high division.
 template <int DT, int MODE, int TDIR, bool TIE = false, bool FLAT = false>
-__device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
-                                            uint64_t* wb, uint32_t* dl, uint32_t t_begin,
-                                            uint32_t t_end, uint32_t n_seg, uint32_t tab) {
+__device__ __forceinline__ uint32_t stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
+                                                uint64_t* wb, uint32_t* dl, uint32_t t_begin,
+                                                uint32_t t_end, uint32_t n_seg, uint32_t tab) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
   constexpr uint32_t kTileBytes = kSegElems * kEsz;
   constexpr uint32_t kSegBlocks = kSegElems / 16;
@@ -622,6 +752,7 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
         fails |= (ok ? 0u : 1u) << j;
       }
     }
+    if (F46_NO_DEFER_PROBE) fails = 0;  // timing probe only (wrong results)
     if (__builtin_expect(__any_sync(0xFFFFFFFFu, fails != 0), 0)) {
       const uint32_t rbk = t * kSegBlocks;
 #pragma unroll
@@ -660,11 +791,10 @@ __device__ __forceinline__ void stream_full(const QParams& p, const TensorConsts
   // one loop body: the stage index is a runtime value
   for (int s = 0; step(s); s ^= 1) parity ^= (uint32_t)s;
 #endif
-  __syncwarp();
-  for (uint32_t i = lane; i < ndefer; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
+  return ndefer;  // the caller resolves the rest of dl[] (one call site per kernel)
 }
 
-template <int DT, int MODE, bool EXTRA>
+template <int DT, int MODE, bool EXTRA, bool PAR = false>
 __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParams p) {
   constexpr int kEsz = (DT == DT_BF16) ? 2 : 4;
   constexpr int kTileBytes = kSegElems * kEsz;
@@ -781,6 +911,7 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   const uint32_t per = total / G, rem = total - per * G;
   const uint32_t t_begin = gw * per + min(gw, rem);
   const uint32_t t_end = t_begin + per + (gw < rem ? 1u : 0u);
+  uint32_t nd = 0;  // deferred blocks stream_full left in dl[]
   if (tc.force_exact) {
     // alpha outside the fast path's range / rule != mse: every block exactly
     const ExactArgs ea{p.x, p.codes, p.scales_tc, p.scales_rm, p.pick4, p.cols, MODE, p.rule};
@@ -794,36 +925,36 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
         case 4:
           if constexpr (MODE == ADAPTIVE) {
             if (tie)
-              stream_full<DT, MODE, 4, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              stream_full<DT, MODE, 4, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case -1:
-          stream_full<DT, MODE, -1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, -1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
           if (tie)
-            stream_full<DT, MODE, 0, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           else
-            stream_full<DT, MODE, 0, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 3:
           if constexpr (MODE == ADAPTIVE) {
             if (tie)
-              stream_full<DT, MODE, 3, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              stream_full<DT, MODE, 3, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case 1:
-          stream_full<DT, MODE, 1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         default:
-          stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
       }
     } else {
-      stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+      nd = stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if (full && F46_FULL) {
     if constexpr (DT == DT_BF16) {
@@ -831,36 +962,36 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
         case 4:
           if constexpr (MODE == ADAPTIVE) {
             if (e4m3_ties_possible(tc.alpha))
-              stream_full<DT, MODE, 4, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              stream_full<DT, MODE, 4>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case -1:
-          stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
           if (MODE == ADAPTIVE && e4m3_ties_possible(tc.alpha))
-            stream_full<DT, MODE, 0, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           else
-            stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 3:
           if constexpr (MODE == ADAPTIVE) {
             if (e4m3_ties_possible(tc.alpha))
-              stream_full<DT, MODE, 3, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              stream_full<DT, MODE, 3>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case 1:
-          stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         default:
-          stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
       }
     } else {
-      stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+      nd = stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if constexpr (DT == DT_BF16) {
     switch (t3 ? 3 : tc.tdir) {
@@ -889,6 +1020,14 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
     }
   } else {
     seg_stream<DT, MODE, EXTRA, 2>(p, tc, wsm, wb, dl, t_begin, t_end, tab);
+  }
+  __syncwarp();
+  if (nd) {
+    const ExactArgs ea{p.x, p.codes, p.scales_tc, nullptr, nullptr, p.cols, MODE, p.rule};
+    if constexpr (PAR)
+      resolve_list<DT, MODE>(ea, tc, kb4, p.d_flags, dl, nd);
+    else
+      for (uint32_t i = lane; i < nd; i += 32) resolve_block_global<DT, MODE>(ea, tc, dl[i], kb4, p.d_flags);
   }
   // tcgen05 layout padding: kb in [nb, 4*kb4) of every row, rows up to a multiple of 128
   const uint32_t rows = (uint32_t)p.rows, rows_pad = (rows + 127) & ~127u;
@@ -2960,12 +3099,29 @@ int launch_status() {
   return F46_OK;
 }
 
+template <int DT, int MODE, bool EXTRA, bool PAR>
+int launch_quant_seg_kernel(const QParams& p, cudaStream_t s, int smem, int ctas_per_sm, int groups = 1);
+
 template <int DT, int MODE, bool EXTRA>
 int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
   constexpr int kTileBytes = kSegElems * ((DT == DT_BF16) ? 2 : 4);
   const int smem = kWarps * kStages * kTileBytes;
   const int ctas_per_sm =
       f46rt::configure((const void*)quant_seg_kernel<DT, MODE, EXTRA>, smem, kWarps * 32);
+  if constexpr (!EXTRA && F46_PAR_RESOLVE) {
+    // small tensors: the instantiation whose end-of-range deferred blocks are
+    // resolved 16 lanes per block (its hot loop spills; large tensors keep the
+    // serial resolver)
+    if (groups == 1 && p.rows * p.cols * ((DT == DT_BF16) ? 2 : 4) <= kParResolveMaxBytes) {
+      const int cps = f46rt::configure((const void*)quant_seg_kernel<DT, MODE, false, true>, smem, kWarps * 32);
+      return launch_quant_seg_kernel<DT, MODE, false, true>(p, s, smem, cps);
+    }
+  }
+  return launch_quant_seg_kernel<DT, MODE, EXTRA, false>(p, s, smem, ctas_per_sm, groups);
+}
+
+template <int DT, int MODE, bool EXTRA, bool PAR>
+int launch_quant_seg_kernel(const QParams& p, cudaStream_t s, int smem, int ctas_per_sm, int groups) {
   QParams pm = p;
   udiv_magic((uint32_t)std::max<int64_t>(1, p.cols >> 4), &pm.nb_magic, &pm.nb_sh1, &pm.nb_sh2);
   // The kernel keeps 32-bit byte offsets: launch at most 2^31 input bytes at a
@@ -2983,7 +3139,7 @@ int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
     int64_t grid = ((int64_t)num_sms() * ctas_per_sm + groups - 1) / groups;
     grid = std::min(grid, (tiles + kWarps - 1) / kWarps);
     if (grid < 1) grid = 1;
-    quant_seg_kernel<DT, MODE, EXTRA><<<dim3((unsigned)grid, (unsigned)groups), kWarps * 32, smem, s>>>(pm);
+    quant_seg_kernel<DT, MODE, EXTRA, PAR><<<dim3((unsigned)grid, (unsigned)groups), kWarps * 32, smem, s>>>(pm);
     return launch_status();
   }
   for (int64_t r0 = 0; r0 < p.rows; r0 += rows_max) {
@@ -2998,7 +3154,7 @@ int launch_quant_seg(const QParams& p, cudaStream_t s, int groups = 1) {
     int64_t grid = (tiles + kWarps - 1) / kWarps;
     if (grid > (int64_t)num_sms() * ctas_per_sm) grid = (int64_t)num_sms() * ctas_per_sm;
     if (grid < 1) grid = 1;
-    quant_seg_kernel<DT, MODE, EXTRA><<<(unsigned)grid, kWarps * 32, smem, s>>>(q);
+    quant_seg_kernel<DT, MODE, EXTRA, PAR><<<(unsigned)grid, kWarps * 32, smem, s>>>(q);
   }
   return launch_status();
 }
@@ -3218,7 +3374,7 @@ int f46_quantize_fused(const void* x, int dtype, int64_t rows, int64_t cols, int
     return F46_OK;
   };
   const int smem_bf16 = kWarps * kStages * kSegElems * 2, smem_f32 = kWarps * kStages * kSegElems * 4;
-#define F46_FUSED(DTV, MV, SMEM) launch((const void*)quant_seg_kernel<DTV, MV, false>, SMEM)
+#define F46_FUSED(DTV, MV, SMEM) launch((const void*)quant_seg_kernel<DTV, MV, false, F46_PAR_RESOLVE != 0>, SMEM)
   if (dtype == F46_DT_BF16) {
     switch (mode) {
       case F46_FIXED6: return F46_FUSED(DT_BF16, FIXED6, smem_bf16);
