@@ -102,7 +102,7 @@ def wgrad_ref(a_bf16: torch.Tensor, spec, mode):
 
 
 @pytest.mark.parametrize("mode", ["adaptive", "fixed6"])
-@pytest.mark.parametrize("T,H", [(256, 320), (3072, 192), (64, 70), (48, 2688)])
+@pytest.mark.parametrize("T,H", [(256, 320), (3072, 192), (64, 70), (48, 2688), (96, 200), (32, 8)])
 def test_wgrad_operand_grouped_oracle(mode, T, H):
     E = 3
     a = bf16_stack(E, (T, H), T + H, [1.0, 1e-3, 2.5])
