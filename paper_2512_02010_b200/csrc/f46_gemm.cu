@@ -692,18 +692,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         const int s = it % kStagesPair;
         const int b = it % kSfBufs;
         mbar_wait(&sf_ld_full[s], (it / kStagesPair) & 1);
-        // buffer b was last read by the MMAs of iteration it - kSfBufs, whose
-        // completion the (multicast) commit on that iteration's `empty` signals
-        if (it >= kSfBufs) {
-          const int prev = it - kSfBufs;
-          mbar_wait(&empty[prev % kStagesPair], (prev / kStagesPair) & 1);
-        }
-        tc_fence_after();
-#if F46_GEMM_DEBUG == 6
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(leader_sf_full + 8 * b);
-        continue;
-#endif
         // SFA: row 32q+lane, k-group j = word q of atom j, row `lane`
         const uint8_t* sa = sm_sfa + s * PSFA_BYTES + lane * 16 + q * 4;
         uint32_t va[16];
@@ -726,6 +714,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             vb[8 * j + 4 * t2 + 3] = w.w;
           }
         }
+        // buffer b was last read by the MMAs of iteration it - kSfBufs, whose
+        // completion the (multicast) commit on that iteration's `empty` signals;
+        // the scale words are already in registers when it arrives
+        if (it >= kSfBufs) {
+          const int prev = it - kSfBufs;
+          mbar_wait(&empty[prev % kStagesPair], (prev / kStagesPair) & 1);
+        }
+        tc_fence_after();
+#if F46_GEMM_DEBUG == 6
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_sf_full + 8 * b);
+        continue;
+#endif
         const uint32_t tsfa = lane_taddr + TM_SF + b * TM_SF_BUF;
 #if F46_SFA_DIAG
         // the MMA reads row block q's SFA from this quadrant at column 4j + q
