@@ -243,6 +243,13 @@ constexpr int64_t kParResolveMaxBytes = (int64_t)96 << 20;
 #define F46_SF_UNROLL 4
 #endif
 constexpr int kSfUnroll = F46_SF_UNROLL;
+// the small-tensor (parallel-resolver) instantiation: a rolled block loop
+// keeps its hot code small, which matters when each warp streams only a few
+// tiles and the instruction cache is cold
+#ifndef F46_SF_UNROLL_SMALL
+#define F46_SF_UNROLL_SMALL 1
+#endif
+constexpr int kSfUnrollSmall = F46_SF_UNROLL_SMALL;
 #ifndef F46_T4
 #define F46_T4 1
 #endif
@@ -677,7 +684,7 @@ __device__ __forceinline__ void seg_stream(const QParams& p, const TensorConsts&
 // sequence (blocks never straddle rows), so tile t is blocks [128t, 128t+128)
 // of it whatever the row length -- no partial per-row segments -- and each
 // block's (row, kb) for the scale layout comes from a multiply-high division.
-template <int DT, int MODE, int TDIR, bool TIE = false, bool FLAT = false>
+template <int DT, int MODE, int TDIR, bool TIE = false, bool FLAT = false, bool SMALL = false>
 __device__ __forceinline__ uint32_t stream_full(const QParams& p, const TensorConsts& tc, uint32_t wsm,
                                                 uint64_t* wb, uint32_t* dl, uint32_t t_begin,
                                                 uint32_t t_end, uint32_t n_seg, uint32_t tab) {
@@ -724,7 +731,7 @@ __device__ __forceinline__ uint32_t stream_full(const QParams& p, const TensorCo
     const uint32_t blk0 = wsm + S * kTileBytes + lane * (16 * kEsz);
     const uint32_t soff = srow + seg * (kSegBlocks / 4) * 512;
     uint32_t fails = 0;
-#pragma unroll kSfUnroll
+#pragma unroll (SMALL ? kSfUnrollSmall : kSfUnroll)
     for (int j = 0; j < kBPL; ++j) {
       const uint32_t blk_addr = blk0 + j * (32 * 16 * kEsz);
       float2 x[8];
@@ -925,36 +932,36 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
         case 4:
           if constexpr (MODE == ADAPTIVE) {
             if (tie)
-              nd = stream_full<DT, MODE, 4, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, true, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              nd = stream_full<DT, MODE, 4, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case -1:
-          nd = stream_full<DT, MODE, -1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, -1, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
           if (tie)
-            nd = stream_full<DT, MODE, 0, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, true, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           else
-            nd = stream_full<DT, MODE, 0, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 3:
           if constexpr (MODE == ADAPTIVE) {
             if (tie)
-              nd = stream_full<DT, MODE, 3, true, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, true, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              nd = stream_full<DT, MODE, 3, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case 1:
-          nd = stream_full<DT, MODE, 1, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 1, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         default:
-          nd = stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 2, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
       }
     } else {
-      nd = stream_full<DT, MODE, 2, false, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+      nd = stream_full<DT, MODE, 2, false, true, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if (full && F46_FULL) {
     if constexpr (DT == DT_BF16) {
@@ -962,36 +969,36 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
         case 4:
           if constexpr (MODE == ADAPTIVE) {
             if (e4m3_ties_possible(tc.alpha))
-              nd = stream_full<DT, MODE, 4, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, true, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              nd = stream_full<DT, MODE, 4>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 4, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case -1:
-          nd = stream_full<DT, MODE, -1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, -1, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 0:
           if (MODE == ADAPTIVE && e4m3_ties_possible(tc.alpha))
-            nd = stream_full<DT, MODE, 0, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, true, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           else
-            nd = stream_full<DT, MODE, 0>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+            nd = stream_full<DT, MODE, 0, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         case 3:
           if constexpr (MODE == ADAPTIVE) {
             if (e4m3_ties_possible(tc.alpha))
-              nd = stream_full<DT, MODE, 3, true>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, true, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
             else
-              nd = stream_full<DT, MODE, 3>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+              nd = stream_full<DT, MODE, 3, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           }
           break;
         case 1:
-          nd = stream_full<DT, MODE, 1>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 1, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
           break;
         default:
-          nd = stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+          nd = stream_full<DT, MODE, 2, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
       }
     } else {
-      nd = stream_full<DT, MODE, 2>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
+      nd = stream_full<DT, MODE, 2, false, false, PAR>(p, tc, wsm, wb, dl, t_begin, t_end, n_seg, tab);
     }
   } else if constexpr (DT == DT_BF16) {
     switch (t3 ? 3 : tc.tdir) {
