@@ -310,6 +310,21 @@ struct TensorConsts {
 // Hence q = t*beta/alpha and the reference's exact-real rounding goes down if
 // alpha > beta, up if alpha < beta and to even if alpha == beta -- one sign for
 // the whole tensor, decided exactly here (alpha*mcap has <= 29 bits).
+// Scale codes, same setting (BF16 x, alpha computed from the amax A): the
+// E4M3 code of a block is RN(bmax/(alpha*m)).  With beta = A/mcap, q_beta =
+// bmax*mcap/(A*m) = (Xb * c * 2^k) / (Xa * m') with Xb, Xa the 8-bit bf16
+// significands, c the odd part of mcap and m' the odd part of m (1 or 3).  An
+// E4M3 tie t has an odd significand T <= 31 (subnormal ties included), so
+// q_beta != t implies |q_beta - t| >= t / (T * Xa * m') >= t * 2^-14.6, while
+// the bracketing products bmax*r_lo, bmax*r_hi lie within 2^-17 of q_alpha and
+// |q_alpha/q_beta - 1| <= 2^-24.  A bracket straddling a tie therefore means
+// an exact tie of q_beta, and q_alpha = t*beta/alpha rounds the way
+// tie_direction says: down for -1 (the lower bracket's code is exact), up for
+// +1 (the upper one's).  For 0 the exact ties need ties-to-even
+// (e4m3_ties_possible / scale_tie).  The K2 prologue collapses the brackets.
+#ifndef F46_SCALE_TDIR
+#define F46_SCALE_TDIR 1
+#endif
 __device__ __forceinline__ int tie_direction(double alpha, double amax, double mcap, int dtype,
                                              bool overridden) {
   if (dtype != DT_BF16 || overridden || !(amax > 0.0)) return 2;
@@ -343,6 +358,21 @@ __device__ __forceinline__ TensorConsts make_consts(double alpha_d, int rule, in
   t.r6_hi = r6 * (1.0f + F46_BRACKET);
   t.r4_lo = r4 * (1.0f - F46_BRACKET);
   t.r4_hi = r4 * (1.0f + F46_BRACKET);
+  return t;
+}
+
+// The K2 streaming kernel's constants for a tensor with tie direction -1 or
+// +1: both scale brackets collapse onto the one whose code is exact (see
+// "Scale codes" above), so no block is deferred for its scale code.
+__device__ __forceinline__ TensorConsts scale_dir_consts(TensorConsts t) {
+  if (F46_SCALE_TDIR) {
+    const bool up = t.tdir == 1, down = t.tdir == -1;
+    const float r6l = t.r6_lo, r4l = t.r4_lo;
+    t.r6_lo = up ? t.r6_hi : t.r6_lo;
+    t.r4_lo = up ? t.r4_hi : t.r4_lo;
+    t.r6_hi = down ? r6l : t.r6_hi;
+    t.r4_hi = down ? r4l : t.r4_hi;
+  }
   return t;
 }
 

@@ -876,9 +876,9 @@ __global__ void __launch_bounds__(kWarps * 32, F46_MINB) quant_seg_kernel(QParam
   const double alpha_d = resolve_alpha(p);
   prologue_flags(p, alpha_d);
   const bool overridden = p.alpha_override > 0.0;
-  const TensorConsts tc = make_consts(
+  const TensorConsts tc = scale_dir_consts(make_consts(
       alpha_d, p.rule, DT,
-      tie_direction(alpha_d, overridden ? 0.0 : __ldcg(p.d_amax), p.mcap, DT, overridden));
+      tie_direction(alpha_d, overridden ? 0.0 : __ldcg(p.d_amax), p.mcap, DT, overridden)));
 
   // per-tensor table of the per-scale-code reciprocals (block46)
   __shared__ __align__(16) float4 sctab[128];

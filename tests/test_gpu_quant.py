@@ -305,3 +305,42 @@ def test_fused_single_launch_equals_two_kernels(shape, dtype, mode):
     ref = O.quantize(bits(x.cpu()) if dtype == torch.bfloat16 else x.cpu().numpy(), mode)
     assert float(a1.item()) == ref["alpha"]
     assert np.array_equal(c1.cpu().numpy(), ref["codes"])
+
+
+def scale_tie_tensor(amax: float, seed: int) -> torch.Tensor:
+    """512x4096 BF16 whose block maxima sit on exact E4M3 ties of the
+    unrounded scale amax/mcap for every mode: significands 7*(17..31) and
+    49, 63 (adaptive, amax = 7*2^e) and 17..31 (fixed6), at several binades."""
+    g = torch.Generator().manual_seed(seed)
+    x = torch.rand(512, 4096, generator=g) * 2.0 - 1.0
+    sig = torch.tensor([7 * t for t in range(17, 32, 2)] + [49, 63] + list(range(17, 32, 2)),
+                       dtype=torch.float32)
+    nb = 512 * 256
+    pick = sig[torch.randint(0, len(sig), (nb,), generator=g)]
+    expo = torch.randint(-14, -7, (nb,), generator=g).float()
+    sgn = torch.where(torch.rand(nb, generator=g) < 0.5, -1.0, 1.0)
+    bmax = sgn * pick * torch.exp2(expo) * (amax / 7.0)
+    xb = x.view(nb, 16) * bmax.abs().unsqueeze(1) * 0.9
+    xb[:, 0] = bmax
+    x = xb.view(512, 4096).to(torch.bfloat16)
+    x[7, 100] = amax
+    return x
+
+
+@pytest.mark.parametrize("mode", ["adaptive", "fixed6", "fixed4"])
+@pytest.mark.parametrize("amax", [7.0, 3.5, 0.109375, 5.25, 6.5])
+def test_scale_code_ties_follow_tie_direction(mode, amax):
+    """Block scales on exact E4M3 ties of the unrounded tensor scale: the
+    streaming kernel settles them by the tensor-wide tie direction (no
+    deferral); codes and scales equal the oracle's bit for bit."""
+    x = scale_tie_tensor(amax, int(amax * 1000))
+    cfg = f46.QuantConfig(scale_mode=mode)
+    q = f46.quantize_tensor_adaptive(x.cuda(), cfg) if mode == "adaptive" else \
+        f46.quantize_tensor(x.cuda(), cfg)
+    ref = O.quantize(bits(x), mode)
+    assert q.alpha == ref["alpha"]
+    got = q.packed_codes.cpu().numpy()
+    bad = np.argwhere(got != ref["codes"])
+    assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[:4].tolist()}"
+    sc = f46.blockquant.tc_to_rowmajor(q.scales_tc, 512, 256).cpu().numpy()
+    assert np.array_equal(sc, ref["scales"].reshape(512, -1))
