@@ -879,14 +879,23 @@ __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const 
   const float2 tl = __fmul2_rn(b2, make_float2(tc.r6_lo, tc.r4_lo));
   const uint32_t ph = cvt_e4m3x2(th.y, th.x);
   uint32_t pl = cvt_e4m3x2(tl.y, tl.x);
-  if (TIE && __builtin_expect(ph != pl, 0)) {
-    // bmax/(alpha*m) within 2^-17 of an E4M3 tie for a candidate: settle the
-    // scale code exactly in place (block_scale_code's test) instead of
-    // deferring the block -- frequent when alpha has few significant bits
-    const uint32_t lo6 = pl & 0xFFu, lo4 = (pl >> 8) & 0xFFu;
-    const uint32_t s6 = lo6 != (ph & 0xFFu) ? scale_tie(lo6, bmax, tc.alpha, 6.f) : lo6;
-    const uint32_t s4 = lo4 != ((ph >> 8) & 0xFFu) ? scale_tie(lo4, bmax, tc.alpha, 4.f) : lo4;
-    pl = s6 | (s4 << 8);
+  if (TIE) {
+#if F46_SCALE_TDIR
+    // alpha has few significant bits and tie direction 0 (alpha = beta): a
+    // bracket disagreement is an exact tie ("Scale codes" above), so the
+    // reference's ties-to-even takes the even code of the two -- the upper
+    // byte wherever the lower one is odd (equal bytes: either)
+    const uint32_t odd = (pl & 0x0101u) * 0xFFu;
+    pl = (pl & ~odd) | (ph & odd);
+#else
+    if (__builtin_expect(ph != pl, 0)) {
+      // settle the scale code exactly in place (block_scale_code's test)
+      const uint32_t lo6 = pl & 0xFFu, lo4 = (pl >> 8) & 0xFFu;
+      const uint32_t s6 = lo6 != (ph & 0xFFu) ? scale_tie(lo6, bmax, tc.alpha, 6.f) : lo6;
+      const uint32_t s4 = lo4 != ((ph >> 8) & 0xFFu) ? scale_tie(lo4, bmax, tc.alpha, 4.f) : lo4;
+      pl = s6 | (s4 << 8);
+    }
+#endif
   }
   if (!TIE) ok &= (ph == pl);
 #if F46_TAB
