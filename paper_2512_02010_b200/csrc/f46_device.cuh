@@ -950,5 +950,9 @@ __device__ __forceinline__ bool block46(const float2 (&x)[8], float bmax, const 
 __device__ __host__ __forceinline__ int64_t sf_tc_offset(int64_t r, int64_t kb, int64_t kb4) {
   return ((r >> 7) * kb4 + (kb >> 2)) * 512 + (r & 31) * 16 + ((r & 127) >> 5) * 4 + (kb & 3);
 }
+// the same in 32-bit arithmetic (scale tables below 4 GB)
+__device__ __forceinline__ uint32_t sf_tc_offset32(uint32_t r, uint32_t kb, uint32_t kb4) {
+  return ((r >> 7) * kb4 + (kb >> 2)) * 512u + (r & 31u) * 16u + ((r & 127u) >> 5) * 4u + (kb & 3u);
+}
 
 }  // namespace f46

@@ -1413,7 +1413,7 @@ __global__ void __launch_bounds__(256, F46_Q2_MINB) quant2d_kernel(Q2Params p) {
     if (r < p.R) {
       reinterpret_cast<uint32_t*>(p.codes + r * nbC * 8)[2 * tc + tc_half] = w;
       if (tc_half == 0) {
-        p.scales_tc[sf_tc_offset(r, tc, kb4)] = (uint8_t)s;
+        p.scales_tc[sf_tc_offset32((uint32_t)r, (uint32_t)tc, (uint32_t)kb4)] = (uint8_t)s;
         if (p.scales_rm) p.scales_rm[r * nbC + tc] = (uint8_t)s;
         if (p.pick4) p.pick4[r * nbC + tc] = (uint8_t)k4;
       }
@@ -1540,12 +1540,26 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
       tie_direction(alpha, overridden ? 0.0 : *p.d_amax, p.mcap, p.dtype, overridden));
   const int64_t G = (int64_t)gridDim.x * (blockDim.x >> 5) * 2;
   bool nonfinite = false;
+  // the half-warp's tile (row tr, column tc), advanced by G tiles per
+  // iteration without a division (tile counts fit 32 bits)
+  const uint32_t tc32 = (uint32_t)TC, gq = (uint32_t)G / tc32, gr = (uint32_t)G - gq * tc32;
+  uint32_t ttr, ttc;
+  {
+    const uint32_t t_first = (uint32_t)(((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + hw);
+    ttr = t_first / tc32;
+    ttc = t_first - ttr * tc32;
+  }
   for (int64_t t0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2; t0 < ntiles;
        t0 += G) {
     const int64_t tile = t0 + hw;
     const bool live = tile < ntiles;
-    // (tile counts fit 32 bits: a 32-bit division, not the 64-bit one)
-    const int64_t tr = live ? (int64_t)((uint32_t)tile / (uint32_t)TC) : 0, tc = live ? tile - tr * TC : 0;
+    const int64_t tr = live ? (int64_t)ttr : 0, tc = live ? (int64_t)ttc : 0;
+    ttc += gr;
+    ttr += gq;
+    if (ttc >= tc32) {
+      ttc -= tc32;
+      ++ttr;
+    }
     const int64_t r0 = tr * 16 + 8 * h, c0 = tc * 16;
     // the lane's 16 values in accumulation order: (row r0 + i/2, col (i%2)*8 + j)
     float x[16];
@@ -1691,22 +1705,25 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
     const bool ok = fast || zero;
     // W rows: lane (h, j) writes row r0 + j; column c's nibble comes from lane
     // (h, c % 8), element 2j + c / 8
-    uint64_t wrow = 0;
+    // byte j of lane (h, c)'s codes = its elements 2j (low nibble) and 2j + 1
+    uint32_t wlo = 0, whi = 0;
+    const uint32_t bsel = (uint32_t)(j & 3) | 0x4440u;  // byte j%4 into byte 0, zeros above
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const uint32_t lo = __shfl_sync(FULL, (uint32_t)codes, hbase + 8 * h + c);
       const uint32_t hi = __shfl_sync(FULL, (uint32_t)(codes >> 32), hbase + 8 * h + c);
-      const uint64_t src = ((uint64_t)hi << 32) | lo;
-      wrow |= ((src >> (8 * j)) & 0xFull) << (4 * c);            // element 2j: column c
-      wrow |= ((src >> (8 * j + 4)) & 0xFull) << (4 * (c + 8));  // element 2j + 1: column 8 + c
+      const uint32_t b = __byte_perm(j < 4 ? lo : hi, 0u, bsel);
+      wlo |= (b & 0xFu) << (4 * c);   // element 2j: column c
+      whi |= (b >> 4) << (4 * c);     // element 2j + 1: column 8 + c
     }
+    const uint64_t wrow = ((uint64_t)whi << 32) | wlo;
     if (live && ok) {
       const int64_t r = r0 + j;
       if (r < p.R) {
         uint64_t w = wrow;
         if (c0 + 16 > p.C) w &= (1ull << (4 * (int)(p.C - c0))) - 1;  // pad columns
         *reinterpret_cast<uint64_t*>(p.codes + (r * nbC + tc) * 8) = w;
-        p.scales_tc[sf_tc_offset(r, tc, kb4)] = (uint8_t)s;
+        p.scales_tc[sf_tc_offset32((uint32_t)r, (uint32_t)tc, (uint32_t)kb4)] = (uint8_t)s;
         if (p.scales_rm) p.scales_rm[r * nbC + tc] = (uint8_t)s;
         if (p.pick4) p.pick4[r * nbC + tc] = (uint8_t)(zero ? (p.mode == FIXED4) : k4);
       }
@@ -1727,7 +1744,7 @@ __global__ void __launch_bounds__(256, F46_Q2V2_MINB) quant2d_v2_kernel(Q2Params
           if (rt < p.C && r0 < p.R) {
             if (r0 + 8 > p.R) wt &= (1u << (4 * (int)(p.R - r0))) - 1u;  // pad rows of W
             reinterpret_cast<uint32_t*>(p.codes_t + (rt * nbR + tr) * 8)[h] = wt;
-            if (h == 0) p.scales_tc_t[sf_tc_offset(rt, tr, kb4t)] = (uint8_t)s;
+            if (h == 0) p.scales_tc_t[sf_tc_offset32((uint32_t)rt, (uint32_t)tr, (uint32_t)kb4t)] = (uint8_t)s;
           } else if (rt < p.C) {
             reinterpret_cast<uint32_t*>(p.codes_t + (rt * nbR + tr) * 8)[h] = 0u;
           }
@@ -3474,6 +3491,9 @@ int f46_quantize_2d_grouped(const void* w, int dtype, int groups, int64_t R, int
              (int64_t)f46_codes_bytes(C, R), (int64_t)f46_scales_tc_bytes(C, R)};
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t tiles = ((R + 15) / 16) * ((C + 15) / 16);
+  // per group, tile indices and scale offsets stay in 32 bits (quant2d_v2_kernel)
+  if (tiles >= (1LL << 31) || R * ((C + 15) / 16) >= (1LL << 31) || C * ((R + 15) / 16) >= (1LL << 31))
+    return F46_ERR_UNSUPPORTED;
   int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
   g2 = std::min<int64_t>(g2, std::max<int64_t>(1, (int64_t)num_sms() * 8 / groups));
   if (rule == F46_RULE_MSE)
@@ -3572,7 +3592,10 @@ int f46_quantize_2d(const void* w, int dtype, int64_t R, int64_t C, int mode, in
   const int64_t cap = (int64_t)num_sms() * 8;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  if (dtype != F46_DT_F64 && !f46rt::hook(f46rt::HOOK_Q2_V1)) {
+  // the v2 kernel keeps tile indices and scale offsets in 32 bits
+  const bool fits32 = tiles < (1LL << 31) && R * ((C + 15) / 16) < (1LL << 31) &&
+                      C * ((R + 15) / 16) < (1LL << 31);
+  if (dtype != F46_DT_F64 && fits32 && !f46rt::hook(f46rt::HOOK_Q2_V1)) {
     int64_t g2 = (tiles + 15) / 16;  // 8 warps x 2 tiles per CTA
     const int64_t cap2 = (int64_t)num_sms() * 8;
     if (g2 > cap2) g2 = cap2;
