@@ -35,5 +35,16 @@ f46.selection_stats(torch.randn(128, 256, device=dev), cfg)
 f46.quantize_block(torch.randn(37).numpy(), 0.01, 6.0)
 f46.emulated_fp4_matmul(f46.quantize_tensor_adaptive(torch.randn(40, 64, device=dev), cfg),
                         f46.quantize_tensor_adaptive(torch.randn(64, 48, device=dev), cfg))
+# K2 through the two-kernel path (parallel-resolver instantiation) on a tensor
+# whose tie direction is +1 (collapsed scale brackets), and a chunked launch
+from paper_2512_02010_b200.sharded import ShardedQuantizer
+xs = torch.randn(256, 4096, device=dev).to(torch.bfloat16)
+xs[3, 5] = 7.0
+sq = ShardedQuantizer(256, 4096, torch.bfloat16, dev, "adaptive", all_reduce_max=lambda t: None)
+sq(xs)
+_lib.load().f46_set_test_hook(_lib.HOOK["seg_chunk_bytes"], 128 * 4096 * 2)
+sq.amax_local(xs, torch.cuda.current_stream().cuda_stream)
+sq.quantize_local(xs, torch.cuda.current_stream().cuda_stream)
+_lib.load().f46_set_test_hook(_lib.HOOK["seg_chunk_bytes"], 0)
 torch.cuda.synchronize()
 print("sanitize workload done")
