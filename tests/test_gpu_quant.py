@@ -344,3 +344,51 @@ def test_scale_code_ties_follow_tie_direction(mode, amax):
     assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[:4].tolist()}"
     sc = f46.blockquant.tc_to_rowmajor(q.scales_tc, 512, 256).cpu().numpy()
     assert np.array_equal(sc, ref["scales"].reshape(512, -1))
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_parallel_resolver_special_blocks(fused, dtype):
+    """Small tensors resolve their deferred blocks 16 lanes per block (odd and
+    even list lengths, special blocks: all-zero with signed zeros, values
+    below the fast path's range, near-ties of every kind); fused and
+    two-kernel launches both equal the oracle bit for bit."""
+    from paper_2512_02010_b200 import _lib
+    from paper_2512_02010_b200.blockquant import scales_tc_bytes, tc_to_rowmajor
+    rows, cols = 384, 2048
+    g = torch.Generator().manual_seed(77)
+    x = torch.randn(rows, cols, generator=g)
+    nb = rows * cols // 16
+    xb = x.view(nb, 16)
+    kind = torch.randint(0, 6, (nb,), generator=g)
+    xb[kind == 0] = 0.0
+    xb[kind == 1] = -0.0
+    xb[kind == 2] *= 1e-13          # bmax below 2^-40: exact path
+    xb[kind == 3] = torch.round(xb[kind == 3] * 4) / 4  # many values on the FP4 grid / ties
+    x[5, 7] = 6.0
+    x = x.to(dtype)
+    ref = O.quantize(bits(x) if dtype == torch.bfloat16 else x.numpy(), "adaptive")
+    L = _lib.load()
+    dt = _lib.DT_BF16 if dtype == torch.bfloat16 else _lib.DT_F32
+    xc = x.cuda()
+    codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device="cuda")
+    sc = torch.zeros(scales_tc_bytes(rows, cols), dtype=torch.uint8, device="cuda")
+    alpha = torch.empty(1, dtype=torch.float64, device="cuda")
+    work = torch.zeros(2, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    if fused:
+        assert L.f46_quantize_fused(xc.data_ptr(), dt, rows, cols, _lib.MODE["adaptive"], 0, 1536.0,
+                                    work.data_ptr(), codes.data_ptr(), sc.data_ptr(),
+                                    alpha.data_ptr(), None, s) == 0
+    else:
+        assert L.f46_amax(xc.data_ptr(), dt, xc.numel(), work.data_ptr(), s) == 0
+        assert L.f46_quantize(xc.data_ptr(), dt, rows, cols, _lib.MODE["adaptive"], 0, 1536.0,
+                              work.data_ptr(), 0.0, codes.data_ptr(), sc.data_ptr(), None, None,
+                              alpha.data_ptr(), None, s) == 0
+    torch.cuda.synchronize()
+    assert float(alpha.item()) == ref["alpha"]
+    got = codes.cpu().numpy()
+    bad = np.argwhere(got != ref["codes"])
+    assert bad.size == 0, f"{len(bad)} code bytes differ, first at {bad[:4].tolist()}"
+    rm = tc_to_rowmajor(sc, rows, cols // 16).cpu().numpy()
+    assert np.array_equal(rm, ref["scales"].reshape(rows, -1))
