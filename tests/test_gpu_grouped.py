@@ -143,3 +143,14 @@ def test_wgrad_operand_matches_linear_wgrad_path():
         assert torch.equal(gq.group(e).packed_codes, q.packed_codes)
         assert torch.equal(gq.group(e).scales_tc, q.scales_tc)
         assert float(gq.group(e).alpha_dev.item()) == q.alpha
+
+
+def test_quantize_grouped_scale_ties_mixed_directions():
+    """Experts whose tensor scales round up, down and exactly, each with block
+    maxima on exact E4M3 ties of its own unrounded scale, in one grouped launch."""
+    from tests.test_gpu_quant import scale_tie_tensor
+    amaxes = (7.0, 6.5, 5.25, 0.109375)
+    x = torch.stack([scale_tie_tensor(a, 5 + i) for i, a in enumerate(amaxes)])
+    gq = f46.quantize_grouped(x.cuda(), f46.QuantConfig(scale_mode="adaptive"))
+    for e in range(len(amaxes)):
+        check_group(gq, e, O.quantize(bits(x[e]), "adaptive"), 512, 4096)
